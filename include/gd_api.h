@@ -1,0 +1,160 @@
+/*
+ * gd_api.h -- C ABI of libgdgpu.so, the B200 (sm_100a) edge-centric graphlet
+ * census.  This is the drop-in boundary for the reference's counting entry
+ * points; every function below names the reference interface it replaces.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Host pointers unless a GD_*_DEVICE flag
+ *     says the buffer is device memory.
+ *   - Every call is synchronous: the library's stream is synchronised before
+ *     return and no caller pointer is retained.
+ *   - Return value: GD_OK (0) or a negative status; gd_last_error() returns a
+ *     thread-local message for the last failure on the calling thread.
+ *   - Wide sums are returned as 13 (lo, hi) uint64 pairs per graph in the
+ *     reference's CensusSums.FIELDS order (census.py:377-378):
+ *       tri, star, indep3, clique4, cycle4, n_tt, n_susv, n_ts, n_ss_same,
+ *       n_ti, n_si, n_ii, outside
+ *     value = lo + 2**64 * hi (the reference keeps Python ints; SPEC.md:211
+ *     mandates 128-bit accumulators).
+ *   - Per-edge rows are int64 [m][10] in canonical edge order with columns
+ *     RAW_MICRO_FIELDS (census.py:95-97):
+ *       tri, star_u, star_v, clique4, cycle4, uu1, vv1, ts1, ti1, si1
+ */
+#ifndef GD_API_H
+#define GD_API_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define GD_API __attribute__((visibility("default")))
+#else
+#define GD_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (mapped to the reference error hierarchy by the host layer) */
+#define GD_OK             0
+#define GD_EINVAL        -1  /* bad argument or invalid sanitized graph   -> ValueError          */
+#define GD_EPARSE        -2  /* vertex id out of declared range / <0      -> EdgeListParseError  */
+#define GD_ECAPACITY     -3  /* size beyond device-path limits            -> GraphSizeError      */
+#define GD_ECUDA         -4  /* CUDA runtime / launch failure             -> DeviceError         */
+#define GD_ECONSISTENCY  -5  /* on-device identity failed (seen != m ...) -> ConsistencyError    */
+
+/* id conventions of gd_graph_create (graph.py:118-157 and 68-114) */
+#define GD_IDS_REMAP      0  /* Graph.from_edges default: dense remap by ascending original id      */
+#define GD_IDS_DECLARED   1  /* ParseOptions.num_vertices / _declared_n: ids must lie in [0, n)     */
+#define GD_IDS_MAX_ID     2  /* ParseOptions.use_max_id: n = max id + 1                              */
+#define GD_IDS_SANITIZED  3  /* Graph(n, edges): no loops/duplicates allowed (ValueError otherwise) */
+
+/* flags */
+#define GD_INPUT_DEVICE   1  /* input pairs / table pointer is device memory   */
+#define GD_OUTPUT_DEVICE  2  /* per-edge table pointer is device memory        */
+
+#define GD_NUM_SUMS       13
+#define GD_NUM_MICRO      10
+
+typedef struct gd_graph gd_graph;  /* opaque, device-resident graph */
+
+GD_API const char* gd_last_error(void);
+GD_API int gd_version(void);
+GD_API int gd_device_ok(void);              /* 1 if a CUDA device is usable, else 0 */
+
+/*
+ * Graph construction on the device.  Replaces Graph.from_edges
+ * (graph.py:118-157) + Graph.__init__ (graph.py:68-114): drop self-loops,
+ * canonicalise (min, max), dedupe, dense remap by ascending original id (or
+ * the declared-n / max-id conventions), degrees, and the degree-ordered
+ * relabelled CSR the counting kernels use.  `pairs` is int64 [k][2].
+ * `n` is the declared vertex count for GD_IDS_DECLARED / GD_IDS_SANITIZED
+ * and ignored otherwise.
+ */
+GD_API int gd_graph_create(const int64_t* pairs, int64_t k, int64_t n, int ids_mode,
+                    int flags, gd_graph** out);
+
+/*
+ * Batched construction for many independent small graphs in one device
+ * graph (disjoint union).  Replaces the per-graph loop of feature_matrix
+ * (analytics.py:111-128).  Graph g owns pairs [pair_offsets[g],
+ * pair_offsets[g+1]) with ids in [0, n_per_graph[g]) (declared-n semantics).
+ */
+GD_API int gd_graph_create_batch(const int64_t* pairs, const int64_t* pair_offsets,
+                          const int64_t* n_per_graph, int64_t num_graphs,
+                          int flags, gd_graph** out);
+
+/* n, m and number of graphs of a device graph (batched: totals) */
+GD_API int gd_graph_info(const gd_graph* g, int64_t* n, int64_t* m, int64_t* num_graphs);
+
+/* per-graph n and m (arrays of length num_graphs); either may be NULL */
+GD_API int gd_graph_sizes(const gd_graph* g, int64_t* n_per_graph, int64_t* m_per_graph);
+
+/*
+ * Export the reference Graph arrays (graph.py:83-114) to host memory; any
+ * pointer may be NULL.  edges int64[m][2] canonical (u<v, lexicographic);
+ * orig_ids int64[n]; indptr int64[n+1]; indices int64[2m] (rows strictly
+ * sorted); edge_slot_ids int64[2m]; degrees int64[n].
+ */
+GD_API int gd_graph_export(const gd_graph* g, int64_t* edges, int64_t* orig_ids,
+                    int64_t* indptr, int64_t* indices, int64_t* edge_slot_ids,
+                    int64_t* degrees);
+
+GD_API void gd_graph_free(gd_graph* g);
+
+/*
+ * Global census.  Replaces graphlet_census (census.py:478-491) ->
+ * run_batches/_census_batch/_count_edge (census.py:437-466, 259-303).
+ * sums: uint64 [num_graphs][13][2]; edges_seen: int64 [num_graphs] (the
+ * reference's `seen == m` check, census.py:489-490, counted on device).
+ */
+GD_API int gd_census_global(gd_graph* g, uint64_t* sums, int64_t* edges_seen);
+
+/*
+ * Per-edge census.  Replaces micro_table (census.py:503-518) ->
+ * _micro_batch/_micro_edge (census.py:469-475, 190-256).  table: int64
+ * [m][10] canonical order (host, or device with GD_OUTPUT_DEVICE); sums and
+ * edges_seen as for gd_census_global (may be NULL).
+ */
+GD_API int gd_census_per_edge(gd_graph* g, int64_t* table, int flags, uint64_t* sums,
+                       int64_t* edges_seen);
+
+/*
+ * Dual route.  Replaces frequencies_from_micro (census.py:521-544): the 13
+ * wide sums of a per-edge table of one graph with n vertices.
+ */
+GD_API int gd_sums_from_table(const int64_t* table, int64_t m, int64_t n, int flags,
+                       uint64_t* sums);
+
+/*
+ * One-shot convenience entries with the signatures a ctypes/cffi binding of
+ * graphlet_census / micro_table binds (sanitized canonical edges of a
+ * reference Graph: g.edges, g.m, g.n).
+ */
+GD_API int gd_census_global_edges(const int64_t* edges, int64_t m, int64_t n, int flags,
+                           uint64_t* sums, int64_t* edges_seen);
+GD_API int gd_census_per_edge_edges(const int64_t* edges, int64_t m, int64_t n, int flags,
+                             int64_t* table, uint64_t* sums, int64_t* edges_seen);
+
+/*
+ * Device timings (CUDA events on the library stream) of the phases of the
+ * last census call on `g`, in milliseconds.  names receives a static,
+ * '\n'-separated list of phase names.  Returns the number of phases written.
+ */
+GD_API int gd_graph_timings(const gd_graph* g, float* ms, int capacity, const char** names);
+
+/* work statistics of the last census call (wedges, triangles, ...) */
+GD_API int gd_graph_stats(const gd_graph* g, int64_t* values, int capacity, const char** names);
+
+/* Pinned host memory helpers (for end-to-end runs without torch). */
+GD_API void* gd_host_alloc(int64_t bytes);
+GD_API void  gd_host_free(void* p);
+
+/* Write a buffer larger than L2 on the library stream (timing hygiene). */
+GD_API int gd_flush_l2(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GD_API_H */

@@ -1,0 +1,5 @@
+"""TEST INFRASTRUCTURE ONLY: the CPU oracle for parity checks.
+
+Importable only from tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs.  The product package never imports it.
+"""

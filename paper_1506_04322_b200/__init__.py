@@ -1,0 +1,38 @@
+"""B200-native edge-centric graphlet census (arXiv 1506.04322).
+
+Drop-in for the counting entry points of the reference package ``graphlets``
+(graphlets/__init__.py:10-56): same names, signatures, result types and
+error classes, with the per-edge counting, the schedule and the reductions
+running as hand-written sm_100a kernels in libgdgpu.so (C ABI:
+include/gd_api.h).  There is no CPU fallback.
+"""
+
+from .analytics import FeatureMatrix, GfdVector, feature_matrix, gfd
+from .census import (RAW_MICRO_FIELDS, CensusSums, census_batch, close_quads,
+                     close_triads, frequencies_from_micro, frequencies_from_sums,
+                     graphlet_census, last_stats, last_timings, micro_census_table,
+                     micro_table)
+from .classes import (ALL_CLASSES, CLASS_BY_ID, CLASS_IDS, GraphletClass,
+                      classes_for, complement_class)
+from .errors import (ClassificationError, ConsistencyError, DeviceError,
+                     EdgeListParseError, GraphletError, GraphSizeError)
+from .frequencies import GraphletFrequencies
+from .graph import EdgeRef, Graph, GraphBatch, ParseOptions, order_edges_by_degree
+from .parallel import MAX_BATCH_SIZE, ParallelConfig, WorkerFailure
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "FeatureMatrix", "GfdVector", "feature_matrix", "gfd",
+    "RAW_MICRO_FIELDS", "CensusSums", "census_batch", "close_quads", "close_triads",
+    "frequencies_from_micro", "frequencies_from_sums", "graphlet_census", "last_stats",
+    "last_timings", "micro_census_table", "micro_table",
+    "ALL_CLASSES", "CLASS_BY_ID", "CLASS_IDS", "GraphletClass", "classes_for",
+    "complement_class",
+    "ClassificationError", "ConsistencyError", "DeviceError", "EdgeListParseError",
+    "GraphletError", "GraphSizeError",
+    "GraphletFrequencies",
+    "EdgeRef", "Graph", "GraphBatch", "ParseOptions", "order_edges_by_degree",
+    "MAX_BATCH_SIZE", "ParallelConfig", "WorkerFailure",
+    "__version__",
+]

@@ -1,0 +1,167 @@
+"""ctypes binding of libgdgpu.so (C ABI declared in include/gd_api.h).
+
+There is no CPU fallback: if the library or a CUDA device is missing, every
+entry point raises DeviceError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+from .errors import (ConsistencyError, DeviceError, EdgeListParseError,
+                     GraphSizeError)
+
+LIB_PATH = Path(__file__).resolve().parent / "libgdgpu.so"
+
+GD_OK, GD_EINVAL, GD_EPARSE, GD_ECAPACITY, GD_ECUDA, GD_ECONSISTENCY = 0, -1, -2, -3, -4, -5
+GD_IDS_REMAP, GD_IDS_DECLARED, GD_IDS_MAX_ID, GD_IDS_SANITIZED = 0, 1, 2, 3
+GD_INPUT_DEVICE, GD_OUTPUT_DEVICE = 1, 2
+NUM_SUMS, NUM_MICRO = 13, 10
+
+_lib = None
+_lock = threading.Lock()
+
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_u64p = ctypes.POINTER(ctypes.c_uint64)
+_vp = ctypes.c_void_p
+
+# (name, restype, argtypes) of every symbol include/gd_api.h declares
+SIGNATURES = (
+    ("gd_last_error", ctypes.c_char_p, []),
+    ("gd_version", ctypes.c_int, []),
+    ("gd_device_ok", ctypes.c_int, []),
+    ("gd_graph_create", ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                       ctypes.c_int, ctypes.POINTER(_vp)]),
+    ("gd_graph_create_batch", ctypes.c_int, [_vp, _i64p, _i64p, ctypes.c_int64, ctypes.c_int,
+                                             ctypes.POINTER(_vp)]),
+    ("gd_graph_info", ctypes.c_int, [_vp, _i64p, _i64p, _i64p]),
+    ("gd_graph_sizes", ctypes.c_int, [_vp, _i64p, _i64p]),
+    ("gd_graph_export", ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    ("gd_graph_free", None, [_vp]),
+    ("gd_census_global", ctypes.c_int, [_vp, _u64p, _i64p]),
+    ("gd_census_per_edge", ctypes.c_int, [_vp, _vp, ctypes.c_int, _u64p, _i64p]),
+    ("gd_sums_from_table", ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                          _u64p]),
+    ("gd_census_global_edges", ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                              _u64p, _i64p]),
+    ("gd_census_per_edge_edges", ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64,
+                                                ctypes.c_int, _vp, _u64p, _i64p]),
+    ("gd_graph_timings", ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_char_p)]),
+    ("gd_graph_stats", ctypes.c_int, [_vp, _i64p, ctypes.c_int,
+                                      ctypes.POINTER(ctypes.c_char_p)]),
+    ("gd_host_alloc", _vp, [ctypes.c_int64]),
+    ("gd_host_free", None, [_vp]),
+    ("gd_flush_l2", ctypes.c_int, []),
+)
+
+
+def load_library(path: Path | None = None):
+    """Load and type libgdgpu.so (no device call).  Raises DeviceError."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = Path(path) if path else LIB_PATH
+        if not p.exists():
+            raise DeviceError(f"{p} is missing: build it with __graft_entry__.build() "
+                              "(there is no CPU fallback)")
+        try:
+            lib = ctypes.CDLL(str(p))
+        except OSError as exc:
+            raise DeviceError(f"cannot load {p}: {exc}") from exc
+        for name, res, args in SIGNATURES:
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def lib():
+    return _lib if _lib is not None else load_library()
+
+
+def check(rc: int) -> None:
+    if rc == GD_OK:
+        return
+    msg = (lib().gd_last_error() or b"").decode(errors="replace")
+    if rc == GD_EINVAL:
+        raise ValueError(msg)
+    if rc == GD_EPARSE:
+        raise EdgeListParseError(msg)
+    if rc == GD_ECAPACITY:
+        raise GraphSizeError(msg)
+    if rc == GD_ECONSISTENCY:
+        raise ConsistencyError(msg)
+    raise DeviceError(f"libgdgpu error {rc}: {msg}")
+
+
+_device_checked = False
+
+
+def require_device() -> None:
+    global _device_checked
+    if not _device_checked:
+        if not lib().gd_device_ok():
+            raise DeviceError("no CUDA device is visible; the B200 path has no CPU fallback")
+        _device_checked = True
+
+
+def ptr(a: np.ndarray | None, t=ctypes.c_int64):
+    return None if a is None else a.ctypes.data_as(ctypes.POINTER(t))
+
+
+def vptr(a: np.ndarray | None):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+def wide(sums: np.ndarray) -> list[int]:
+    """(lo, hi) uint64 pairs -> Python ints."""
+    s = sums.reshape(-1, 2)
+    return [int(lo) + (int(hi) << 64) for lo, hi in s]
+
+
+class PinnedArray(np.ndarray):
+    """A numpy array whose memory is page-locked host memory from
+    gd_host_alloc; freed when the last view is garbage collected."""
+
+    def __array_finalize__(self, obj):
+        self._pin_owner = getattr(obj, "_pin_owner", None)
+
+
+class _PinOwner:
+    __slots__ = ("p", "free")
+
+    def __init__(self, p, free):
+        self.p = p
+        self.free = free
+
+    def __del__(self):
+        if self.p:
+            self.free(self.p)
+            self.p = None
+
+
+def pinned_empty(shape, dtype=np.int64) -> np.ndarray:
+    dtype = np.dtype(dtype)
+    count = int(np.prod(shape)) if len(shape) else 1
+    nbytes = max(count * dtype.itemsize, 1)
+    L = lib()
+    p = L.gd_host_alloc(nbytes)
+    if not p:
+        return np.empty(shape, dtype=dtype)  # pageable is still correct, only slower
+    buf = (ctypes.c_char * nbytes).from_address(p)
+    arr = np.frombuffer(buf, dtype=dtype, count=count).reshape(shape).view(PinnedArray)
+    arr._pin_owner = _PinOwner(p, L.gd_host_free)
+    return arr
+
+
+def env_flag(name: str) -> bool:
+    return os.environ.get(name, "") not in ("", "0", "false", "False")

@@ -1,0 +1,117 @@
+"""Graph feature vectors and frequency distributions (analytics.py:44-131).
+
+``feature_matrix`` keeps the reference signature, including its plugin seam
+``census_fn``.  Without a ``census_fn`` every graph is counted in ONE batched
+device pass (GraphBatch: disjoint union, per-graph 128-bit sums) instead of
+the reference's serial per-graph loop; the float rows are then built on the
+host exactly as the reference builds them (float(count), log1p, L1 scaling),
+so they are bit-identical.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .census import census_batch, graphlet_census
+from .classes import classes_for
+from .frequencies import GraphletFrequencies
+from .graph import GraphBatch
+from .parallel import ParallelConfig
+
+GFD_SCOPES = ("connected", "all")
+
+
+@dataclass(frozen=True)
+class GfdVector:
+    k: int
+    scope: str
+    class_ids: tuple[str, ...]
+    values: tuple[float, ...]
+    is_zero: bool = False
+
+
+def gfd(freqs: GraphletFrequencies, k: int = 4, scope: str = "connected") -> GfdVector:
+    """Normalised size-k frequencies (analytics.py:44-59)."""
+    if k not in (3, 4):
+        raise ValueError("gfd supports k in {3, 4}")
+    if scope not in GFD_SCOPES:
+        raise ValueError(f"scope must be one of {GFD_SCOPES}")
+    ids = classes_for(k, connected_only=scope == "connected")
+    raw = [freqs.counts[c] for c in ids]
+    total = sum(raw)
+    if total == 0:
+        return GfdVector(k, scope, ids, tuple(0.0 for _ in ids), True)
+    return GfdVector(k, scope, ids, tuple(v / total for v in raw))
+
+
+@dataclass
+class FeatureMatrix:
+    class_ids: tuple[str, ...]
+    labels: list[str]
+    rows: np.ndarray
+    seconds: list[float]
+    skipped: list[tuple[str, str]] = field(default_factory=list)
+
+
+def _row(freqs, class_ids, log_scale, normalize):
+    row = [float(freqs.counts[c]) for c in class_ids]
+    if log_scale:
+        row = [math.log1p(v) for v in row]
+    if normalize:
+        total = sum(row)
+        if total > 0:
+            row = [v / total for v in row]
+    return row
+
+
+def feature_matrix(graphs, labels=None, config: ParallelConfig | None = None,
+                   log_scale: bool = False, normalize: bool = False,
+                   census_fn=None) -> FeatureMatrix:
+    """One 17-dim count row per graph (analytics.py:91-131).  ``graphs`` is a
+    sequence of graph-like objects (n, edges) or a GraphBatch."""
+    class_ids = classes_for(2) + classes_for(3) + classes_for(4)
+    kept, rows, seconds, skipped = [], [], [], []
+    if census_fn is None:
+        batch = graphs if isinstance(graphs, GraphBatch) else None
+        if batch is None:
+            graphs = list(graphs)
+        count = batch.num_graphs if batch is not None else len(graphs)
+        if labels is None:
+            labels = [f"graph_{i}" for i in range(count)]
+        if count == 0:
+            return FeatureMatrix(class_ids, [], np.zeros((0, len(class_ids))), [], [])
+        t0 = time.perf_counter()
+        if batch is None:
+            batch = GraphBatch.from_graphs(graphs)
+        results = census_batch(batch)
+        per = (time.perf_counter() - t0) / count
+        for label, res in zip(labels, results):
+            if isinstance(res, Exception):
+                skipped.append((label, f"{type(res).__name__}: {res}"))
+                continue
+            kept.append(label)
+            rows.append(_row(res, class_ids, log_scale, normalize))
+            seconds.append(per)
+    else:
+        graphs = list(graphs)
+        if labels is None:
+            labels = [f"graph_{i}" for i in range(len(graphs))]
+        for label, g in zip(labels, graphs):
+            t0 = time.perf_counter()
+            try:
+                freqs = census_fn(g, config) if config is not None else census_fn(g)
+            except Exception as exc:  # per-graph failure: record, skip row
+                skipped.append((label, f"{type(exc).__name__}: {exc}"))
+                continue
+            seconds.append(time.perf_counter() - t0)
+            kept.append(label)
+            rows.append(_row(freqs, class_ids, log_scale, normalize))
+    matrix = np.asarray(rows, dtype=np.float64).reshape(len(rows), len(class_ids))
+    return FeatureMatrix(class_ids, kept, matrix, seconds, skipped)
+
+
+__all__ = ["GfdVector", "gfd", "FeatureMatrix", "feature_matrix", "graphlet_census"]

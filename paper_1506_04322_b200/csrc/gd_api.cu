@@ -1,0 +1,355 @@
+// extern "C" boundary of libgdgpu.so (declared in include/gd_api.h).
+#include <cstring>
+#include <mutex>
+
+#include "gd_build.cuh"
+#include "gd_count.cuh"
+
+struct gd_graph {
+  gd::DevGraph g;
+  cudaStream_t s = nullptr;
+  std::vector<float> ms;
+  std::string names;
+  std::vector<int64_t> stats;
+  std::string stats_names;
+};
+
+namespace gd {
+
+static thread_local std::string t_last_error;
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        sms <= 0)
+      sms = 148;
+  }
+  return sms;
+}
+
+static void init_pool_once() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;  // keep freed blocks cached across calls
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
+
+static cudaStream_t thread_stream() {
+  static thread_local cudaStream_t s = nullptr;
+  if (!s) GD_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  return s;
+}
+
+template <typename F>
+static int guarded(F&& f) {
+  try {
+    init_pool_once();
+    f();
+    return GD_OK;
+  } catch (const Error& e) {
+    t_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    t_last_error = "host allocation failed";
+    return GD_ECAPACITY;
+  } catch (const std::exception& e) {
+    t_last_error = e.what();
+    return GD_ECUDA;
+  }
+}
+
+typedef unsigned __int128 u128;
+
+static u128 get128(const unsigned long long* p) { return ((u128)p[1] << 64) | p[0]; }
+static void put128(uint64_t* p, u128 v) {
+  p[0] = (uint64_t)v;
+  p[1] = (uint64_t)(v >> 64);
+}
+
+// Fill in / check the 4-clique and 4-cycle fields from the device totals.
+//   sum_e cl(e) = 6 K4;  sum_e cy(e) = 4 * (#4-cycles - sum_e C(t,2) + 3 K4)
+// (each 4-clique holds 3 four-cycles, each diamond one; diamonds =
+// sum_e C(t,2) - 6 K4, close_quads census.py:399-403).
+static void close_cycles(uint64_t* sums, const CensusExtras& ex, int64_t G, bool per_edge) {
+  for (int64_t i = 0; i < G; i++) {
+    uint64_t* s = sums + i * 2 * kNumSums;
+    const u128 k4 = ex.k4tot[i];
+    const u128 c4x2 = ex.c4tot2[i];
+    if (c4x2 & 1) throw Error(GD_ECONSISTENCY, "odd 4-cycle wedge-pair total");
+    const u128 c4 = c4x2 >> 1;
+    const u128 ntt = get128((const unsigned long long*)(s + 2 * 5));
+    if (get128((const unsigned long long*)(s + 2 * 3)) != 6 * k4)
+      throw Error(GD_ECONSISTENCY, "per-edge 4-clique sum != 6 x enumerated 4-cliques");
+    if (c4 + 3 * k4 < ntt) throw Error(GD_ECONSISTENCY, "negative induced 4-cycle count");
+    const u128 cy = 4 * (c4 + 3 * k4 - ntt);
+    if (per_edge) {
+      if (get128((const unsigned long long*)(s + 2 * 4)) != cy)
+        throw Error(GD_ECONSISTENCY, "per-edge 4-cycle sum != 4 x enumerated 4-cycles");
+    } else {
+      put128(s + 2 * 4, cy);
+    }
+  }
+}
+
+static void store_timings(gd_graph* h, CensusExtras& ex) {
+  h->ms = ex.ms;
+  h->names.clear();
+  for (auto& n : ex.names) h->names += n + "\n";
+  h->stats = ex.stats;
+  h->stats_names.clear();
+  for (auto& n : ex.stats_names) h->stats_names += n + "\n";
+}
+
+static void census(gd_graph* h, bool per_edge, int64_t* table, int flags, uint64_t* sums,
+                   int64_t* seen) {
+  DevGraph& g = h->g;
+  cudaStream_t s = h->s;
+  const int64_t G = g.G;
+  DBuf<unsigned long long> dsums, dseen;
+  dsums.alloc(G * 2 * kNumSums, s);
+  dseen.alloc(G, s);
+  DBuf<long long> dtable;
+  long long* tptr = nullptr;
+  if (per_edge && table) {
+    if (flags & GD_OUTPUT_DEVICE) {
+      tptr = (long long*)table;
+    } else {
+      dtable.alloc((size_t)g.m * kNumMicro, s);
+      tptr = dtable.p;
+    }
+  }
+  CensusExtras ex;
+  run_census(g, per_edge, tptr, dsums.p, dseen.p, ex, s);
+  std::vector<uint64_t> hs(G * 2 * kNumSums);
+  std::vector<int64_t> hseen(G);
+  GD_CUDA(cudaMemcpyAsync(hs.data(), dsums.p, hs.size() * 8, cudaMemcpyDeviceToHost, s));
+  GD_CUDA(cudaMemcpyAsync(hseen.data(), dseen.p, G * 8, cudaMemcpyDeviceToHost, s));
+  if (dtable.p && g.m)
+    GD_CUDA(cudaMemcpyAsync(table, dtable.p, (size_t)g.m * kNumMicro * 8, cudaMemcpyDeviceToHost,
+                            s));
+  GD_CUDA(cudaStreamSynchronize(s));
+  store_timings(h, ex);
+  close_cycles(hs.data(), ex, G, per_edge);
+  if (sums) std::memcpy(sums, hs.data(), hs.size() * 8);
+  if (seen) std::memcpy(seen, hseen.data(), G * 8);
+}
+
+}  // namespace gd
+
+using namespace gd;
+
+extern "C" {
+
+const char* gd_last_error(void) { return t_last_error.c_str(); }
+
+int gd_version(void) { return 1; }
+
+int gd_device_ok(void) {
+  int c = 0;
+  return (cudaGetDeviceCount(&c) == cudaSuccess && c > 0) ? 1 : 0;
+}
+
+int gd_graph_create(const int64_t* pairs, int64_t k, int64_t n, int ids_mode, int flags,
+                    gd_graph** out) {
+  if (!out) {
+    t_last_error = "out is NULL";
+    return GD_EINVAL;
+  }
+  *out = nullptr;
+  if (k > 0 && !pairs) {
+    t_last_error = "pairs is NULL";
+    return GD_EINVAL;
+  }
+  gd_graph* h = new gd_graph();
+  int rc = guarded([&] {
+    GD_CUDA(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+    build_graph(h->g, pairs, k, n, ids_mode, flags, h->s);
+  });
+  if (rc != GD_OK) {
+    gd_graph_free(h);
+    return rc;
+  }
+  *out = h;
+  return GD_OK;
+}
+
+int gd_graph_create_batch(const int64_t* pairs, const int64_t* pair_offsets,
+                          const int64_t* n_per_graph, int64_t num_graphs, int flags,
+                          gd_graph** out) {
+  if (!out || !pair_offsets || !n_per_graph) {
+    t_last_error = "NULL argument";
+    return GD_EINVAL;
+  }
+  *out = nullptr;
+  gd_graph* h = new gd_graph();
+  int rc = guarded([&] {
+    GD_CUDA(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+    build_graph_batch(h->g, pairs, pair_offsets, n_per_graph, num_graphs, flags, h->s);
+  });
+  if (rc != GD_OK) {
+    gd_graph_free(h);
+    return rc;
+  }
+  *out = h;
+  return GD_OK;
+}
+
+int gd_graph_info(const gd_graph* h, int64_t* n, int64_t* m, int64_t* num_graphs) {
+  if (!h) {
+    t_last_error = "NULL graph";
+    return GD_EINVAL;
+  }
+  if (n) *n = h->g.n;
+  if (m) *m = h->g.m;
+  if (num_graphs) *num_graphs = h->g.G;
+  return GD_OK;
+}
+
+int gd_graph_sizes(const gd_graph* h, int64_t* n_per_graph, int64_t* m_per_graph) {
+  if (!h) {
+    t_last_error = "NULL graph";
+    return GD_EINVAL;
+  }
+  for (int64_t i = 0; i < h->g.G; i++) {
+    if (n_per_graph) n_per_graph[i] = h->g.h_gn[i];
+    if (m_per_graph) m_per_graph[i] = h->g.h_eoff[i + 1] - h->g.h_eoff[i];
+  }
+  return GD_OK;
+}
+
+int gd_graph_export(const gd_graph* h, int64_t* edges, int64_t* orig_ids, int64_t* indptr,
+                    int64_t* indices, int64_t* edge_slot_ids, int64_t* degrees) {
+  if (!h) {
+    t_last_error = "NULL graph";
+    return GD_EINVAL;
+  }
+  return guarded([&] {
+    export_graph(h->g, edges, orig_ids, indptr, indices, edge_slot_ids, degrees, h->s);
+  });
+}
+
+void gd_graph_free(gd_graph* h) {
+  if (!h) return;
+  if (h->s) cudaStreamSynchronize(h->s);
+  {
+    // release device buffers before the stream goes away
+    gd::DevGraph empty;
+    std::swap(h->g, empty);
+  }
+  if (h->s) {
+    cudaStreamSynchronize(h->s);
+    cudaStreamDestroy(h->s);
+  }
+  delete h;
+}
+
+int gd_census_global(gd_graph* h, uint64_t* sums, int64_t* edges_seen) {
+  if (!h) {
+    t_last_error = "NULL graph";
+    return GD_EINVAL;
+  }
+  return guarded([&] { census(h, false, nullptr, 0, sums, edges_seen); });
+}
+
+int gd_census_per_edge(gd_graph* h, int64_t* table, int flags, uint64_t* sums,
+                       int64_t* edges_seen) {
+  if (!h) {
+    t_last_error = "NULL graph";
+    return GD_EINVAL;
+  }
+  return guarded([&] { census(h, true, table, flags, sums, edges_seen); });
+}
+
+int gd_sums_from_table(const int64_t* table, int64_t m, int64_t n, int flags, uint64_t* sums) {
+  if ((m > 0 && !table) || !sums || m < 0) {
+    t_last_error = "bad argument";
+    return GD_EINVAL;
+  }
+  return guarded([&] {
+    cudaStream_t s = thread_stream();
+    DBuf<long long> dt;
+    const long long* tp = (const long long*)table;
+    if (!(flags & GD_INPUT_DEVICE) && m) {
+      dt.alloc((size_t)m * kNumMicro, s);
+      GD_CUDA(cudaMemcpyAsync(dt.p, table, (size_t)m * kNumMicro * 8, cudaMemcpyHostToDevice, s));
+      tp = dt.p;
+    }
+    DBuf<unsigned long long> ds;
+    ds.alloc(2 * kNumSums, s);
+    sums_from_table(tp, m, n, ds.p, s);
+    GD_CUDA(cudaMemcpyAsync(sums, ds.p, 2 * kNumSums * 8, cudaMemcpyDeviceToHost, s));
+    GD_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int gd_census_global_edges(const int64_t* edges, int64_t m, int64_t n, int flags, uint64_t* sums,
+                           int64_t* edges_seen) {
+  gd_graph* h = nullptr;
+  int rc = gd_graph_create(edges, m, n, GD_IDS_SANITIZED, flags & GD_INPUT_DEVICE, &h);
+  if (rc != GD_OK) return rc;
+  rc = gd_census_global(h, sums, edges_seen);
+  gd_graph_free(h);
+  return rc;
+}
+
+int gd_census_per_edge_edges(const int64_t* edges, int64_t m, int64_t n, int flags,
+                             int64_t* table, uint64_t* sums, int64_t* edges_seen) {
+  gd_graph* h = nullptr;
+  int rc = gd_graph_create(edges, m, n, GD_IDS_SANITIZED, flags & GD_INPUT_DEVICE, &h);
+  if (rc != GD_OK) return rc;
+  rc = gd_census_per_edge(h, table, flags & GD_OUTPUT_DEVICE, sums, edges_seen);
+  gd_graph_free(h);
+  return rc;
+}
+
+int gd_graph_timings(const gd_graph* h, float* ms, int capacity, const char** names) {
+  if (!h) return 0;
+  int k = (int)std::min<size_t>(h->ms.size(), (size_t)std::max(capacity, 0));
+  for (int i = 0; i < k; i++) ms[i] = h->ms[i];
+  if (names) *names = h->names.c_str();
+  return k;
+}
+
+int gd_graph_stats(const gd_graph* h, int64_t* values, int capacity, const char** names) {
+  if (!h) return 0;
+  int k = (int)std::min<size_t>(h->stats.size(), (size_t)std::max(capacity, 0));
+  for (int i = 0; i < k; i++) values[i] = h->stats[i];
+  if (names) *names = h->stats_names.c_str();
+  return k;
+}
+
+void* gd_host_alloc(int64_t bytes) {
+  void* p = nullptr;
+  if (bytes <= 0) return nullptr;
+  if (cudaHostAlloc(&p, (size_t)bytes, cudaHostAllocDefault) != cudaSuccess) {
+    t_last_error = "cudaHostAlloc failed";
+    return nullptr;
+  }
+  return p;
+}
+
+void gd_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int gd_flush_l2(void) {
+  return guarded([&] {
+    static void* buf = nullptr;
+    const size_t bytes = 256ull << 20;  // 2x the 126 MB L2
+    cudaStream_t s = thread_stream();
+    if (!buf) GD_CUDA(cudaMalloc(&buf, bytes));
+    GD_CUDA(cudaMemsetAsync(buf, (int)(rand() & 0xff), bytes, s));
+    GD_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,184 @@
+"""Generate the golden vectors of tests/golden/ by running the REFERENCE.
+
+Run in the build container only (it imports /root/reference/pkg/src, which
+does not exist on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [--c2]
+
+Outputs (committed):
+  small_graphs.json  reference graphlet_census + micro_table on the reference
+                     test-suite graph families (canonical graphs, zoo, G(n,p)
+                     corpus, degenerate n, beyond-64-bit case)
+  c1.npz / configs.json   config 1 (ER 2000/10000): reference counts, the full
+                     reference micro_table, and sha256 fingerprints of the
+                     generated pairs and of the reference-sanitised edges
+  c4_batch.npz       reference feature_matrix counts of all 4096 config-4
+                     graphs (int64, 17 columns)
+  c2 (with --c2)     config 2 global counts + micro_table sha256 and sampled
+                     rows (the full reference per-edge run takes ~10 min on 8
+                     cores)
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+sys.path.insert(0, str(REF))
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parent.parent))
+
+import graphlets as R  # noqa: E402  (the reference)
+from graphlets import generate as RG  # noqa: E402
+from graphlets.analytics import feature_matrix  # noqa: E402
+
+from paper_1506_04322_b200 import workloads as W  # noqa: E402
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def counts_json(f) -> dict:
+    return {k: str(int(v)) for k, v in f.counts.items()}
+
+
+def small_cases():
+    cases = []
+    canon = {
+        "K3": RG.complete_graph(3), "K4": RG.complete_graph(4), "C4": RG.cycle_graph(4),
+        "C5": RG.cycle_graph(5), "P4": RG.path_graph(4), "K1,3": RG.star_graph(3),
+        "K1,5": RG.star_graph(5), "diamond": RG.diamond_graph(), "paw": RG.paw_graph(),
+        "2K2": RG.two_disjoint_edges_graph(), "K5+pendant": RG.clique_plus_pendant(5),
+    }
+    cases += list(canon.items())
+    for n in (0, 1, 2, 3):
+        cases.append((f"empty{n}", RG.empty_graph(n)))
+    # zoo (test_census.py:406-456 families)
+    rng = np.random.default_rng(7)
+    for seed in range(3):
+        a, b = 6, 8
+        r = np.random.default_rng(seed)
+        e = [(i, a + j) for i in range(a) for j in range(b) if r.random() < 0.4]
+        cases.append((f"bipartite{seed}", R.Graph(a + b, np.asarray(e, dtype=np.int64).reshape(-1, 2))))
+    for seed in range(3):
+        r = np.random.default_rng(seed)
+        e = [(int(r.integers(0, v)), v) for v in range(1, 24)]
+        cases.append((f"tree{seed}", R.Graph(24, np.asarray(e, dtype=np.int64))))
+    grid = []
+    for rr in range(4):
+        for cc in range(5):
+            v = rr * 5 + cc
+            if cc + 1 < 5:
+                grid.append((v, v + 1))
+            if rr + 1 < 4:
+                grid.append((v, v + 5))
+    cases.append(("grid4x5", R.Graph(20, np.asarray(grid, dtype=np.int64))))
+    cases.append(("tri+17isolated", R.Graph(20, np.asarray([[0, 1], [1, 2], [2, 0]]))))
+    q3 = [(a, b) for a in range(8) for b in range(a + 1, 8) if bin(a ^ b).count("1") == 1]
+    cases.append(("Q3", R.Graph(8, np.asarray(q3, dtype=np.int64))))
+    for seed in range(3):
+        cases.append((f"dense_complement{seed}",
+                      R.complement(RG.gnp_random_graph(14, 0.2, seed=seed))))
+    cases.append(("beyond64", R.Graph(200_000, np.asarray([[0, 1], [1, 2], [5, 6]]))))
+    # G(n, p) corpus in the style of test_acceptance.py:43-56
+    probs = np.arange(1, 10) / 10
+    for i in range(120):
+        n = int(rng.integers(4, 41))
+        p = float(rng.choice(probs))
+        cases.append((f"G({n},{p:.1f})#{i}", RG.gnp_random_graph(n, p, seed=int(rng.integers(1 << 31)))))
+    # a few denser, larger ones with hubs
+    for i in range(6):
+        cases.append((f"BA(200,{i + 2})", RG.powerlaw_cluster_graph(200, i + 2, seed=i)))
+    return cases
+
+
+def make_small():
+    out = []
+    for name, g in small_cases():
+        f = R.graphlet_census(g)
+        if g.n <= 30:
+            assert f == R.oracle_census(g), name
+        tab = R.micro_table(g)
+        out.append({"name": name, "n": g.n, "edges": g.edges.tolist(),
+                    "counts": counts_json(f), "micro": tab.tolist()})
+    (HERE / "small_graphs.json").write_text(json.dumps(out))
+    print("small graphs:", len(out))
+
+
+def ref_graph(raw: W.RawGraph):
+    return R.Graph.from_edges(raw.pairs, R.ParseOptions(num_vertices=raw.n))
+
+
+def make_configs(with_c2: bool):
+    cfg_path = HERE / "configs.json"
+    configs = json.loads(cfg_path.read_text()) if cfg_path.exists() else {}
+    workers = os.cpu_count()
+    names = ["c1_er"] + (["c2_chung_lu"] if with_c2 else [])
+    for name in names:
+        raw = W.config_graph(name)
+        g = ref_graph(raw)
+        g.adj_lists()
+        g.edge_columns()
+        t0 = time.time()
+        f = R.graphlet_census(g, R.ParallelConfig(workers=workers))
+        t_glob = time.time() - t0
+        t0 = time.time()
+        tab = R.micro_table(g, R.ParallelConfig(workers=workers))
+        t_micro = time.time() - t0
+        assert R.frequencies_from_micro(g, tab) == f
+        rng = np.random.default_rng(99)
+        sample = np.sort(rng.choice(g.m, size=min(g.m, 512), replace=False))
+        configs[name] = {
+            "n": g.n, "m": g.m,
+            "pairs_sha256": sha(raw.pairs), "edges_sha256": sha(g.edges),
+            "counts": counts_json(f), "micro_sha256": sha(tab),
+            "sample_idx": sample.tolist(), "sample_rows": tab[sample].tolist(),
+            "reference_seconds": {"graphlet_census": t_glob, "micro_table": t_micro,
+                                  "workers": workers},
+        }
+        if name == "c1_er":
+            np.savez_compressed(HERE / "c1.npz", micro=tab, edges=g.edges.astype(np.int32))
+        print(name, g.n, g.m, f"global {t_glob:.1f}s micro {t_micro:.1f}s")
+        cfg_path.write_text(json.dumps(configs, indent=1))
+
+
+def make_batch():
+    raws = W.config_batch()
+    graphs = [ref_graph(r) for r in raws]
+    t0 = time.time()
+    fm = feature_matrix(graphs)
+    dt = time.time() - t0
+    counts = np.asarray([[int(R.graphlet_census(g).counts[c]) for c in R.CLASS_IDS]
+                         for g in graphs[:32]], dtype=np.int64)
+    rows = fm.rows
+    assert np.array_equal(rows[:32], counts.astype(np.float64))
+    exact = np.asarray([[int(x) for x in r] for r in rows], dtype=np.int64)
+    assert np.array_equal(exact.astype(np.float64), rows)
+    np.savez_compressed(HERE / "c4_batch.npz", counts=exact,
+                        n=np.asarray([g.n for g in graphs], dtype=np.int64),
+                        m=np.asarray([g.m for g in graphs], dtype=np.int64))
+    meta_path = HERE / "configs.json"
+    configs = json.loads(meta_path.read_text()) if meta_path.exists() else {}
+    configs["c4_batch"] = {"graphs": len(graphs), "sum_m": int(sum(g.m for g in graphs)),
+                           "sum_n": int(sum(g.n for g in graphs)),
+                           "pairs_sha256": sha(np.concatenate([r.pairs for r in raws])),
+                           "reference_seconds": {"feature_matrix_serial": dt}}
+    meta_path.write_text(json.dumps(configs, indent=1))
+    print("batch", len(graphs), f"{dt:.1f}s")
+
+
+if __name__ == "__main__":
+    if "--small" in sys.argv or len(sys.argv) == 1:
+        make_small()
+    if "--configs" in sys.argv or len(sys.argv) == 1 or "--c2" in sys.argv:
+        make_configs("--c2" in sys.argv)
+    if "--batch" in sys.argv or len(sys.argv) == 1:
+        make_batch()
