@@ -390,6 +390,104 @@ __device__ __forceinline__ int64_t wedge_slot(const int64_t* __restrict__ WP, in
   return lo;
 }
 
+// Wedge iteration.  The items of one frame (or chunk) are split in warp
+// chunks of 32*K consecutive items; lane l handles items c0+l, c0+l+32, ...
+// so lanes of a warp read consecutive entries of the same row w (coalesced)
+// and the slot p of an item is found by one binary search per lane per chunk
+// followed by forward steps (no per-item search).
+constexpr int kWedgeK = 16;
+
+enum WedgeMode { kCount = 0, kUse = 1, kZero = 2, kTake = 3 };
+
+struct SlabCounter {
+  unsigned* cnt;
+  __device__ __forceinline__ void inc(int x) const { atomicAdd(&cnt[x], 1u); }
+  __device__ __forceinline__ unsigned get(int x) const { return cnt[x]; }
+  __device__ __forceinline__ unsigned take(int x) const { return atomicExch(&cnt[x], 0u); }
+  __device__ __forceinline__ void zero(int x) const { cnt[x] = 0u; }
+};
+
+struct HashCounter {
+  int* hk;
+  int* hv;
+  int hmask;
+  __device__ __forceinline__ void inc(int x) const {
+    unsigned h = hash32((unsigned)x) & hmask;
+    while (true) {
+      int old = atomicCAS(&hk[h], -1, x);
+      if (old == -1 || old == x) {
+        atomicAdd(&hv[h], 1);
+        return;
+      }
+      h = (h + 1) & hmask;
+    }
+  }
+  __device__ __forceinline__ unsigned get(int x) const {
+    unsigned h = hash32((unsigned)x) & hmask;
+    while (hk[h] != x) h = (h + 1) & hmask;
+    return (unsigned)hv[h];
+  }
+  __device__ __forceinline__ unsigned take(int x) const { return get(x); }  // unused
+  __device__ __forceinline__ void zero(int) const {}
+};
+
+// Runs one sweep of `mode` over items [i0, i1) of frame s (lower slots
+// [b, o)).  Returns this thread's partial sum (kUse: sum of cnt-1 over its
+// wedges; kTake: sum of c*(c-1) over taken counters).
+template <int NT, int MODE, typename C>
+__device__ unsigned long long wedge_sweep(const View& g, const int64_t* __restrict__ WP,
+                                          int64_t b, int64_t o, int64_t i0, int64_t i1,
+                                          const C& ctr, bool per_edge,
+                                          unsigned long long* __restrict__ c4e) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int nw = NT / 32;
+  constexpr int64_t CH = 32 * kWedgeK;
+  unsigned long long local = 0;
+  for (int64_t c0 = i0 + (int64_t)warp * CH; c0 < i1; c0 += (int64_t)nw * CH) {
+    const int64_t c1 = c0 + CH < i1 ? c0 + CH : i1;
+    int64_t i = c0 + lane;
+    if (i >= c1) continue;
+    int64_t p = wedge_slot(WP, b, o, i);
+    int64_t wp1 = WP[p + 1];
+    int64_t base = g.rp[g.col[p]] - WP[p];  // q = base + i
+    unsigned long long top = 0;             // per-edge: pending sum for edge (s, w_p)
+    for (; i < c1; i += 32) {
+      if (wp1 <= i) {
+        if (MODE == kUse && per_edge && top) {
+          atomicAdd(&c4e[g.seid[p]], top);
+          top = 0;
+        }
+        do {
+          p++;
+          wp1 = WP[p + 1];
+        } while (wp1 <= i);
+        base = g.rp[g.col[p]] - WP[p];
+      }
+      const int64_t q = base + i;
+      const int x = g.col[q];
+      if (MODE == kCount) {
+        ctr.inc(x);
+      } else if (MODE == kZero) {
+        ctr.zero(x);
+      } else if (MODE == kTake) {
+        unsigned long long c = ctr.take(x);
+        local += c * (c - (c > 0));
+      } else {
+        unsigned long long c = ctr.get(x) - 1u;
+        if (c) {
+          local += c;
+          if (per_edge) {
+            atomicAdd(&c4e[g.seid[q]], c);
+            top += c;
+          }
+        }
+      }
+    }
+    if (MODE == kUse && per_edge && top) atomicAdd(&c4e[g.seid[p]], top);
+  }
+  return local;
+}
+
 // Small frames: counters in a shared-memory hash.
 template <int NT>
 __global__ void __launch_bounds__(NT)
@@ -409,26 +507,13 @@ k_c4_frames_smem(View g, const int64_t* __restrict__ WP, const int* __restrict__
     const int64_t total = i1 - i0;
     int H = pow2_at_least((int)(2 * total < (int64_t)hcap ? 2 * total : (int64_t)hcap));
     if (H > hcap) H = hcap;
-    const int hmask = H - 1;
+    HashCounter ctr{hk, hv, H - 1};
     for (int h = threadIdx.x; h < H; h += NT) {
       hk[h] = -1;
       hv[h] = 0;
     }
     __syncthreads();
-    for (int64_t i = i0 + threadIdx.x; i < i1; i += NT) {
-      int64_t p = wedge_slot(WP, b, o, i);
-      int w = g.col[p];
-      int x = g.col[g.rp[w] + (i - WP[p])];
-      unsigned h = hash32((unsigned)x) & hmask;
-      while (true) {
-        int old = atomicCAS(&hk[h], -1, x);
-        if (old == -1 || old == x) {
-          atomicAdd(&hv[h], 1);
-          break;
-        }
-        h = (h + 1) & hmask;
-      }
-    }
+    wedge_sweep<NT, kCount>(g, WP, b, o, i0, i1, ctr, false, c4e);
     __syncthreads();
     unsigned long long local = 0;
     if (!per_edge) {
@@ -437,20 +522,7 @@ k_c4_frames_smem(View g, const int64_t* __restrict__ WP, const int* __restrict__
         local += c * (c - (c > 0));  // 2 * C(c, 2)
       }
     } else {
-      for (int64_t i = i0 + threadIdx.x; i < i1; i += NT) {
-        int64_t p = wedge_slot(WP, b, o, i);
-        int w = g.col[p];
-        int64_t q = g.rp[w] + (i - WP[p]);
-        int x = g.col[q];
-        unsigned h = hash32((unsigned)x) & hmask;
-        while (hk[h] != x) h = (h + 1) & hmask;
-        unsigned long long c = (unsigned)hv[h] - 1u;
-        if (c) {
-          atomicAdd(&c4e[g.seid[q]], c);
-          atomicAdd(&c4e[g.seid[p]], c);
-          local += c;
-        }
-      }
+      local = wedge_sweep<NT, kUse>(g, WP, b, o, i0, i1, ctr, true, c4e);
     }
     unsigned long long sum = BR(tmp).Sum(local);
     if (threadIdx.x == 0 && sum) atomic_add_u128(c4tot2 + 2 * graph_of(g, s), sum);
@@ -459,56 +531,28 @@ k_c4_frames_smem(View g, const int64_t* __restrict__ WP, const int* __restrict__
 }
 
 // Large frames: counters in a dense per-CTA global slab (n u32, zero on entry
-// and restored to zero on exit).  Frames may be split into `chunks` item
-// ranges processed by different CTAs when `shared_slab` (hub mode): then the
-// three sweeps run as three launches (phase 0 count, 1 use, 2 zero).
-__global__ void __launch_bounds__(512)
+// and restored to zero on exit).
+template <int NT>
+__global__ void __launch_bounds__(NT)
 k_c4_frames_slab(View g, const int64_t* __restrict__ WP, const int* __restrict__ frames,
                  int nframes, unsigned* __restrict__ slabs, int64_t slab_stride, int per_edge,
                  unsigned long long* __restrict__ c4e, unsigned long long* __restrict__ c4tot2) {
-  typedef cub::BlockReduce<unsigned long long, 512> BR;
+  typedef cub::BlockReduce<unsigned long long, NT> BR;
   __shared__ typename BR::TempStorage tmp;
-  unsigned* cnt = slabs + (size_t)blockIdx.x * slab_stride;
+  SlabCounter ctr{slabs + (size_t)blockIdx.x * slab_stride};
   for (int f = blockIdx.x; f < nframes; f += gridDim.x) {
     const int s = frames[f];
     const int64_t b = g.rp[s], o = g.osplit[s];
     const int64_t i0 = WP[b], i1 = WP[o];
-    for (int64_t i = i0 + threadIdx.x; i < i1; i += 512) {
-      int64_t p = wedge_slot(WP, b, o, i);
-      int w = g.col[p];
-      int x = g.col[g.rp[w] + (i - WP[p])];
-      atomicAdd(&cnt[x], 1u);
-    }
+    wedge_sweep<NT, kCount>(g, WP, b, o, i0, i1, ctr, false, c4e);
     __syncthreads();
-    unsigned long long local = 0;
+    unsigned long long local;
     if (!per_edge) {
-      for (int64_t i = i0 + threadIdx.x; i < i1; i += 512) {
-        int64_t p = wedge_slot(WP, b, o, i);
-        int w = g.col[p];
-        int x = g.col[g.rp[w] + (i - WP[p])];
-        unsigned long long c = atomicExch(&cnt[x], 0u);
-        local += c * (c - (c > 0));
-      }
+      local = wedge_sweep<NT, kTake>(g, WP, b, o, i0, i1, ctr, false, c4e);
     } else {
-      for (int64_t i = i0 + threadIdx.x; i < i1; i += 512) {
-        int64_t p = wedge_slot(WP, b, o, i);
-        int w = g.col[p];
-        int64_t q = g.rp[w] + (i - WP[p]);
-        int x = g.col[q];
-        unsigned long long c = cnt[x] - 1u;
-        if (c) {
-          atomicAdd(&c4e[g.seid[q]], c);
-          atomicAdd(&c4e[g.seid[p]], c);
-          local += c;
-        }
-      }
+      local = wedge_sweep<NT, kUse>(g, WP, b, o, i0, i1, ctr, true, c4e);
       __syncthreads();
-      for (int64_t i = i0 + threadIdx.x; i < i1; i += 512) {
-        int64_t p = wedge_slot(WP, b, o, i);
-        int w = g.col[p];
-        int x = g.col[g.rp[w] + (i - WP[p])];
-        cnt[x] = 0u;
-      }
+      wedge_sweep<NT, kZero>(g, WP, b, o, i0, i1, ctr, false, c4e);
     }
     unsigned long long sum = BR(tmp).Sum(local);
     if (threadIdx.x == 0 && sum) atomic_add_u128(c4tot2 + 2 * graph_of(g, s), sum);
@@ -516,47 +560,130 @@ k_c4_frames_slab(View g, const int64_t* __restrict__ WP, const int* __restrict__
   }
 }
 
-// Hub frames: each (frame, chunk) is one CTA; frame h uses slab h.
+// Hub frames: each (frame, chunk) is one CTA; frame h uses slab h.  The
+// sweeps are separate launches (phase 0 count, 1 use, 2 zero).
 struct HubChunk {
   int frame;       // rank id s
   int slab;        // slab index
   int64_t i0, i1;  // item range
 };
 
-__global__ void __launch_bounds__(512)
+template <int NT>
+__global__ void __launch_bounds__(NT)
 k_c4_hub(View g, const int64_t* __restrict__ WP, const HubChunk* __restrict__ chunks,
          unsigned* __restrict__ slabs, int64_t slab_stride, int phase, int per_edge,
          unsigned long long* __restrict__ c4e, unsigned long long* __restrict__ c4tot2) {
-  typedef cub::BlockReduce<unsigned long long, 512> BR;
+  typedef cub::BlockReduce<unsigned long long, NT> BR;
   __shared__ typename BR::TempStorage tmp;
   const HubChunk ch = chunks[blockIdx.x];
-  unsigned* cnt = slabs + (size_t)ch.slab * slab_stride;
+  SlabCounter ctr{slabs + (size_t)ch.slab * slab_stride};
   const int s = ch.frame;
   const int64_t b = g.rp[s], o = g.osplit[s];
-  unsigned long long local = 0;
-  for (int64_t i = ch.i0 + threadIdx.x; i < ch.i1; i += 512) {
-    int64_t p = wedge_slot(WP, b, o, i);
-    int w = g.col[p];
-    int64_t q = g.rp[w] + (i - WP[p]);
-    int x = g.col[q];
-    if (phase == 0) {
-      atomicAdd(&cnt[x], 1u);
-    } else if (phase == 1) {
-      unsigned long long c = cnt[x] - 1u;
-      if (c) {
-        if (per_edge) {
-          atomicAdd(&c4e[g.seid[q]], c);
-          atomicAdd(&c4e[g.seid[p]], c);
-        }
-        local += c;
-      }
-    } else {
-      cnt[x] = 0u;
-    }
-  }
-  if (phase == 1) {
+  if (phase == 0) {
+    wedge_sweep<NT, kCount>(g, WP, b, o, ch.i0, ch.i1, ctr, false, c4e);
+  } else if (phase == 1) {
+    unsigned long long local =
+        wedge_sweep<NT, kUse>(g, WP, b, o, ch.i0, ch.i1, ctr, per_edge != 0, c4e);
     unsigned long long sum = BR(tmp).Sum(local);
     if (threadIdx.x == 0 && sum) atomic_add_u128(c4tot2 + 2 * graph_of(g, s), sum);
+  } else {
+    wedge_sweep<NT, kZero>(g, WP, b, o, ch.i0, ch.i1, ctr, false, c4e);
+  }
+}
+
+// Cooperative rounds for the heavy frames.  All CTAs are co-resident
+// (cooperative launch) and walk the same round schedule: a round is up to F
+// frames whose u16 counter slabs (n/2 words each) stay L2-resident; its
+// items are cut into chunks of CH items spread over the whole grid.
+//   step r:  count(round r) + zero(round r-1)  | barrier |  use(round r) | barrier
+// Two slab sets alternate so zeroing round r-1 overlaps counting round r.
+struct U16Counter {
+  unsigned* w;  // 2 counters per 32-bit word
+  __device__ __forceinline__ void inc(int x) const {
+    atomicAdd(&w[x >> 1], 1u << ((x & 1) << 4));
+  }
+  __device__ __forceinline__ unsigned get(int x) const {
+    return ((const unsigned short*)w)[x];
+  }
+  __device__ __forceinline__ unsigned take(int x) const { return get(x); }  // unused
+  __device__ __forceinline__ void zero(int x) const { ((unsigned short*)w)[x] = 0; }
+};
+
+struct RoundPlan {
+  const int* frames;    // heavy frames (rank ids), descending wedges
+  const int64_t* cpre;  // [nf+1] chunk prefix
+  const int* rf;        // [R+1] round -> first frame index
+  int R;                // rounds
+  int F;                // max frames per round (slabs per set)
+  int64_t CH;           // items per chunk
+  int64_t slab_words;   // 32-bit words per slab
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned g = gen;
+    const unsigned arrived = atomicAdd(&bar[0], 1u) + 1u;
+    if (arrived == gridDim.x) {
+      bar[0] = 0u;
+      __threadfence();
+      atomicAdd(&bar[1], 1u);
+    } else {
+      while (*(volatile unsigned*)&bar[1] == g) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  gen++;
+  __syncthreads();
+}
+
+template <int NT, int MODE>
+__device__ void round_chunks(const View& g, const int64_t* __restrict__ WP, const RoundPlan& P,
+                             int r, unsigned* __restrict__ slabs, bool per_edge,
+                             unsigned long long* __restrict__ c4e,
+                             unsigned long long* __restrict__ c4tot2) {
+  typedef cub::BlockReduce<unsigned long long, NT> BR;
+  __shared__ typename BR::TempStorage tmp;
+  const int f0 = P.rf[r], f1 = P.rf[r + 1];
+  const int64_t k0 = P.cpre[f0], k1 = P.cpre[f1];
+  unsigned* set = slabs + (size_t)(r & 1) * P.F * P.slab_words;
+  for (int64_t k = k0 + blockIdx.x; k < k1; k += gridDim.x) {
+    // frame of chunk k: last j in [f0, f1) with cpre[j] <= k
+    int lo = f0, hi = f1;
+    while (lo < hi - 1) {
+      int mid = (lo + hi) >> 1;
+      if (P.cpre[mid] <= k) lo = mid; else hi = mid;
+    }
+    const int j = lo;
+    const int s = P.frames[j];
+    const int64_t b = g.rp[s], o = g.osplit[s];
+    const int64_t fi0 = WP[b], fi1 = WP[o];
+    const int64_t i0 = fi0 + (k - P.cpre[j]) * P.CH;
+    const int64_t i1 = i0 + P.CH < fi1 ? i0 + P.CH : fi1;
+    U16Counter ctr{set + (size_t)(j - f0) * P.slab_words};
+    unsigned long long local = wedge_sweep<NT, MODE>(g, WP, b, o, i0, i1, ctr, per_edge, c4e);
+    if (MODE == kUse) {
+      unsigned long long sum = BR(tmp).Sum(local);
+      if (threadIdx.x == 0 && sum) atomic_add_u128(c4tot2 + 2 * graph_of(g, s), sum);
+      __syncthreads();
+    }
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT)
+k_c4_rounds(View g, const int64_t* __restrict__ WP, RoundPlan P, unsigned* __restrict__ slabs,
+            int per_edge, unsigned long long* __restrict__ c4e,
+            unsigned long long* __restrict__ c4tot2, unsigned* __restrict__ bar) {
+  unsigned gen = 0;
+  for (int r = 0; r <= P.R; r++) {
+    if (r < P.R) round_chunks<NT, kCount>(g, WP, P, r, slabs, false, c4e, c4tot2);
+    if (r > 0) round_chunks<NT, kZero>(g, WP, P, r - 1, slabs, false, c4e, c4tot2);
+    if (r == P.R) break;
+    grid_barrier(bar, gen);
+    round_chunks<NT, kUse>(g, WP, P, r, slabs, per_edge != 0, c4e, c4tot2);
+    grid_barrier(bar, gen);
   }
 }
 
@@ -910,6 +1037,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   GD_CUDA(cudaMemsetAsync(items.p + 2 * m, 0, 8, s));
   exclusive_scan(items.p, WP.p, 2 * m + 1, s);
   items.release();
+  timer.mark("sched_prefix");
 
   DBuf<unsigned long long> fk, fk_sorted, wk_sorted;
   DBuf<int> fid, tri_frames, c4_frames;
@@ -1000,54 +1128,119 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     for (int64_t w : wkeys) total_w += w;
     ex.stats.push_back(total_w);
     ex.stats_names.push_back("wedges");
-    // hub threshold: frames big enough to be split over many CTAs
-    const int64_t hub_t = std::max<int64_t>(1 << 20, total_w / (num_sms() * 4));
-    const int64_t slab_t = 4096;  // > slab_t wedges: dense global slab
-    auto rh = count_range(wkeys, hub_t + 1, INT64_MAX);
-    auto rl = count_range(wkeys, slab_t + 1, hub_t);
+    // Bins by wedges: (coop_t, inf) cooperative rounds with L2-resident u16
+    // slabs (frames whose lower degree < 65536), (slab_t, coop_t] per-CTA
+    // u32 slabs, (256, slab_t] and [1, 256] shared-memory hashes.  Frames
+    // whose counters may exceed 16 bits go through the u32 hub path.
+    const int64_t slab_t = 4096;
+    const int64_t coop_t = std::max<int64_t>(1 << 17, slab_t);
+    auto rh = count_range(wkeys, coop_t + 1, INT64_MAX);
+    auto rl = count_range(wkeys, slab_t + 1, coop_t);
     auto rs1 = count_range(wkeys, 257, slab_t);
     auto rs0 = count_range(wkeys, 1, 256);
     const int64_t slab_stride = (n + 31) & ~int64_t(31);
-    // hubs: groups of up to kMaxHubSlabs frames
     const int64_t nh = rh.second - rh.first;
+    int64_t n_u32_hubs = 0;
     if (nh > 0) {
-      const int64_t max_slabs = std::max<int64_t>(
-          1, std::min<int64_t>(nh, (int64_t)(2ll << 30) / (slab_stride * 4)));
-      DBuf<unsigned> slabs;
-      slabs.alloc((size_t)max_slabs * slab_stride, s);
-      slabs.zero();
+      // heavy frames: split into u16-safe (lower degree < 65536) and u32 hubs
       std::vector<int> hf(nh);
       GD_CUDA(cudaMemcpyAsync(hf.data(), c4_frames.p + rh.first, nh * 4, cudaMemcpyDeviceToHost,
                               s));
-      std::vector<int64_t> rpv(2), WPv(2);
+      std::vector<int64_t> hb(nh), ho(nh);
       GD_CUDA(cudaStreamSynchronize(s));
-      const int64_t chunk_items = 1 << 16;
-      for (int64_t g0 = 0; g0 < nh; g0 += max_slabs) {
-        const int64_t g1 = std::min(nh, g0 + max_slabs);
-        std::vector<HubChunk> chunks;
-        for (int64_t h = g0; h < g1; h++) {
-          const int sframe = hf[h];
-          int64_t b = 0, o = 0, i0 = 0, i1 = 0;
-          GD_CUDA(cudaMemcpyAsync(&b, g.rp.p + sframe, 8, cudaMemcpyDeviceToHost, s));
-          GD_CUDA(cudaMemcpyAsync(&o, g.osplit.p + sframe, 8, cudaMemcpyDeviceToHost, s));
-          GD_CUDA(cudaStreamSynchronize(s));
-          GD_CUDA(cudaMemcpyAsync(&i0, WP.p + b, 8, cudaMemcpyDeviceToHost, s));
-          GD_CUDA(cudaMemcpyAsync(&i1, WP.p + o, 8, cudaMemcpyDeviceToHost, s));
-          GD_CUDA(cudaStreamSynchronize(s));
-          for (int64_t c = i0; c < i1; c += chunk_items)
-            chunks.push_back({sframe, (int)(h - g0), c, std::min(i1, c + chunk_items)});
+      std::vector<int64_t> hrp(n + 1), hos(n);
+      GD_CUDA(cudaMemcpyAsync(hrp.data(), g.rp.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+      GD_CUDA(cudaMemcpyAsync(hos.data(), g.osplit.p, n * 8, cudaMemcpyDeviceToHost, s));
+      GD_CUDA(cudaStreamSynchronize(s));
+      std::vector<int> f16, f32;
+      std::vector<int64_t> w16, w32;
+      for (int64_t h = 0; h < nh; h++) {
+        const int sf = hf[h];
+        if (hos[sf] - hrp[sf] < 65536) {
+          f16.push_back(sf);
+          w16.push_back(wkeys[rh.first + h]);
+        } else {
+          f32.push_back(sf);
+          w32.push_back(wkeys[rh.first + h]);
         }
-        DBuf<HubChunk> dch;
-        dch.alloc(chunks.size(), s);
-        GD_CUDA(cudaMemcpyAsync(dch.p, chunks.data(), chunks.size() * sizeof(HubChunk),
-                                cudaMemcpyHostToDevice, s));
-        for (int phase = 0; phase < 3; phase++) {
-          k_c4_hub<<<(int)chunks.size(), 512, 0, s>>>(v, WP.p, dch.p, slabs.p, slab_stride, phase,
-                                                     per_edge ? 1 : 0, c4e.p, c4tot2.p);
-          GD_LAUNCH_CHECK("c4_hub");
-        }
-        GD_CUDA(cudaStreamSynchronize(s));
       }
+      n_u32_hubs = (int64_t)f32.size();
+      if (!f16.empty()) {
+        const int64_t CH = 8192;
+        const int64_t slab_words = (slab_stride / 2 + 31) & ~int64_t(31);
+        const int64_t l2_budget = 48ll << 20;
+        const int F = (int)std::max<int64_t>(1, std::min<int64_t>(64, l2_budget / (slab_words * 4)));
+        std::vector<int64_t> cpre(f16.size() + 1, 0);
+        for (size_t j = 0; j < f16.size(); j++) cpre[j + 1] = cpre[j] + (w16[j] + CH - 1) / CH;
+        std::vector<int> rf;
+        for (size_t j = 0; j < f16.size(); j += F) rf.push_back((int)j);
+        rf.push_back((int)f16.size());
+        DBuf<int> dfr, drf;
+        DBuf<int64_t> dcp;
+        DBuf<unsigned> slabs, bar;
+        dfr.alloc(f16.size(), s);
+        drf.alloc(rf.size(), s);
+        dcp.alloc(cpre.size(), s);
+        slabs.alloc((size_t)2 * F * slab_words, s);
+        slabs.zero();
+        bar.alloc(2, s);
+        bar.zero();
+        GD_CUDA(cudaMemcpyAsync(dfr.p, f16.data(), f16.size() * 4, cudaMemcpyHostToDevice, s));
+        GD_CUDA(cudaMemcpyAsync(drf.p, rf.data(), rf.size() * 4, cudaMemcpyHostToDevice, s));
+        GD_CUDA(cudaMemcpyAsync(dcp.p, cpre.data(), cpre.size() * 8, cudaMemcpyHostToDevice, s));
+        RoundPlan P{dfr.p, dcp.p, drf.p, (int)rf.size() - 1, F, CH, slab_words};
+        constexpr int NT = 512;
+        int per_sm = 0;
+        GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_c4_rounds<NT>, NT, 0));
+        if (per_sm < 1) throw Error(GD_ECUDA, "c4 rounds kernel cannot be resident");
+        const int grid = per_sm * num_sms();
+        int pe = per_edge ? 1 : 0;
+        unsigned long long* c4e_p = c4e.p;
+        unsigned long long* c4t_p = c4tot2.p;
+        unsigned* slabs_p = slabs.p;
+        unsigned* bar_p = bar.p;
+        const int64_t* WP_p = WP.p;
+        void* args[] = {(void*)&v, (void*)&WP_p, (void*)&P, (void*)&slabs_p, (void*)&pe,
+                        (void*)&c4e_p, (void*)&c4t_p, (void*)&bar_p};
+        GD_CUDA(cudaLaunchCooperativeKernel((void*)k_c4_rounds<NT>, dim3(grid), dim3(NT), args, 0,
+                                            s));
+        GD_LAUNCH_CHECK("c4_rounds");
+        ex.stats.push_back((int64_t)rf.size() - 1);
+        ex.stats_names.push_back("c4_rounds");
+      }
+      timer.mark("c4_coop");
+      if (!f32.empty()) {
+        const int64_t max_slabs = std::max<int64_t>(
+            1, std::min<int64_t>((int64_t)f32.size(), (int64_t)(2ll << 30) / (slab_stride * 4)));
+        DBuf<unsigned> slabs;
+        slabs.alloc((size_t)max_slabs * slab_stride, s);
+        slabs.zero();
+        const int64_t chunk_items = 1 << 16;
+        for (size_t g0 = 0; g0 < f32.size(); g0 += max_slabs) {
+          const size_t g1 = std::min(f32.size(), (size_t)(g0 + max_slabs));
+          std::vector<HubChunk> chunks;
+          for (size_t h = g0; h < g1; h++) {
+            const int sframe = f32[h];
+            int64_t i0 = 0, i1 = 0;
+            GD_CUDA(cudaMemcpyAsync(&i0, WP.p + hrp[sframe], 8, cudaMemcpyDeviceToHost, s));
+            GD_CUDA(cudaMemcpyAsync(&i1, WP.p + hos[sframe], 8, cudaMemcpyDeviceToHost, s));
+            GD_CUDA(cudaStreamSynchronize(s));
+            for (int64_t c = i0; c < i1; c += chunk_items)
+              chunks.push_back({sframe, (int)(h - g0), c, std::min(i1, c + chunk_items)});
+          }
+          DBuf<HubChunk> dch;
+          dch.alloc(chunks.size(), s);
+          GD_CUDA(cudaMemcpyAsync(dch.p, chunks.data(), chunks.size() * sizeof(HubChunk),
+                                  cudaMemcpyHostToDevice, s));
+          for (int phase = 0; phase < 3; phase++) {
+            k_c4_hub<512><<<(int)chunks.size(), 512, 0, s>>>(
+                v, WP.p, dch.p, slabs.p, slab_stride, phase, per_edge ? 1 : 0, c4e.p, c4tot2.p);
+            GD_LAUNCH_CHECK("c4_hub");
+          }
+          GD_CUDA(cudaStreamSynchronize(s));
+        }
+      }
+      timer.mark("c4_hubs32");
     }
     const int64_t nl = rl.second - rl.first;
     if (nl > 0) {
@@ -1055,10 +1248,10 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       DBuf<unsigned> slabs;
       slabs.alloc((size_t)grid * slab_stride, s);
       slabs.zero();
-      k_c4_frames_slab<<<grid, 512, 0, s>>>(v, WP.p, c4_frames.p + rl.first, (int)nl, slabs.p,
+      k_c4_frames_slab<512><<<grid, 512, 0, s>>>(v, WP.p, c4_frames.p + rl.first, (int)nl, slabs.p,
                                             slab_stride, per_edge ? 1 : 0, c4e.p, c4tot2.p);
       GD_LAUNCH_CHECK("c4_frames_slab");
-      GD_CUDA(cudaStreamSynchronize(s));
+      timer.mark("c4_slab");
     }
     const int64_t ns1 = rs1.second - rs1.first;
     if (ns1 > 0) {
@@ -1070,6 +1263,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       k_c4_frames_smem<256><<<grid, 256, sm, s>>>(v, WP.p, c4_frames.p + rs1.first, (int)ns1,
                                                   hcap, per_edge ? 1 : 0, c4e.p, c4tot2.p);
       GD_LAUNCH_CHECK("c4_frames_smem256");
+      timer.mark("c4_smem256");
     }
     const int64_t ns0 = rs0.second - rs0.first;
     if (ns0 > 0) {
@@ -1081,7 +1275,9 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       GD_LAUNCH_CHECK("c4_frames_smem64");
     }
     ex.stats.push_back(nh);
-    ex.stats_names.push_back("hub_frames");
+    ex.stats_names.push_back("coop_frames");
+    ex.stats.push_back(n_u32_hubs);
+    ex.stats_names.push_back("u32_hub_frames");
     ex.stats.push_back(nl);
     ex.stats_names.push_back("slab_frames");
   }
