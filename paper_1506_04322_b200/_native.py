@@ -128,28 +128,25 @@ def wide(sums: np.ndarray) -> list[int]:
     return [int(lo) + (int(hi) << 64) for lo, hi in s]
 
 
-class PinnedArray(np.ndarray):
-    """A numpy array whose memory is page-locked host memory from
-    gd_host_alloc; freed when the last view is garbage collected."""
+class _PinnedBuffer:
+    """Owns page-locked host memory from gd_host_alloc.  Exposed to numpy via
+    __array_interface__, so every numpy view's base chain ends here and the
+    memory is freed only when the last view is gone."""
 
-    def __array_finalize__(self, obj):
-        self._pin_owner = getattr(obj, "_pin_owner", None)
-
-
-class _PinOwner:
-    __slots__ = ("p", "free")
-
-    def __init__(self, p, free):
+    def __init__(self, p: int, nbytes: int, free):
         self.p = p
-        self.free = free
+        self._free = free
+        self.__array_interface__ = {"data": (p, False), "shape": (nbytes,),
+                                    "typestr": "|u1", "version": 3}
 
     def __del__(self):
         if self.p:
-            self.free(self.p)
-            self.p = None
+            self._free(self.p)
+            self.p = 0
 
 
 def pinned_empty(shape, dtype=np.int64) -> np.ndarray:
+    """np.empty in page-locked host memory (fast D2H of per-edge tables)."""
     dtype = np.dtype(dtype)
     count = int(np.prod(shape)) if len(shape) else 1
     nbytes = max(count * dtype.itemsize, 1)
@@ -157,10 +154,8 @@ def pinned_empty(shape, dtype=np.int64) -> np.ndarray:
     p = L.gd_host_alloc(nbytes)
     if not p:
         return np.empty(shape, dtype=dtype)  # pageable is still correct, only slower
-    buf = (ctypes.c_char * nbytes).from_address(p)
-    arr = np.frombuffer(buf, dtype=dtype, count=count).reshape(shape).view(PinnedArray)
-    arr._pin_owner = _PinOwner(p, L.gd_host_free)
-    return arr
+    raw = np.asarray(_PinnedBuffer(p, nbytes, L.gd_host_free))
+    return raw[:count * dtype.itemsize].view(dtype).reshape(shape)
 
 
 def env_flag(name: str) -> bool:

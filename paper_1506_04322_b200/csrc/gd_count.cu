@@ -993,8 +993,31 @@ void launch_trisum(const View& v, const int* frames, int nf, const FrameLayout& 
 // ---------------------------------------------------------------------------
 // Host orchestration
 // ---------------------------------------------------------------------------
+// Test-only schedule overrides (GD_FORCE_PATH=tri_gmem,c4_slab,...): route
+// every frame through one kernel variant so each variant can be checked
+// against the oracle on small graphs.  Results never depend on the path.
+struct ForcePaths {
+  bool tri_gmem = false, tri_small = false, c4_slab = false, c4_coop = false,
+       c4_hub32 = false, c4_smem = false;
+};
+
+static ForcePaths read_force() {
+  ForcePaths f;
+  const char* e = getenv("GD_FORCE_PATH");
+  if (!e) return f;
+  std::string v(e);
+  f.tri_gmem = v.find("tri_gmem") != std::string::npos;
+  f.tri_small = v.find("tri_small") != std::string::npos;
+  f.c4_slab = v.find("c4_slab") != std::string::npos;
+  f.c4_coop = v.find("c4_coop") != std::string::npos;
+  f.c4_hub32 = v.find("c4_hub32") != std::string::npos;
+  f.c4_smem = v.find("c4_smem") != std::string::npos;
+  return f;
+}
+
 void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long long* sums_dev,
                 unsigned long long* seen_dev, CensusExtras& ex, cudaStream_t s) {
+  const ForcePaths force = read_force();
   const int64_t n = g.n, m = g.m, G = g.G;
   const View v = make_view(g);
   Timer timer(s);
@@ -1074,6 +1097,8 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     struct B { int64_t lo, hi; int nt; bool gmem; };
     std::vector<B> bins = {{1025, INT64_MAX, 512, true}, {513, 1024, 512, false},
                            {129, 512, 256, false}, {33, 128, 128, false}, {2, 32, 32, false}};
+    if (force.tri_gmem) bins = {{2, INT64_MAX, 512, true}};
+    if (force.tri_small) bins = {{2, INT64_MAX, 32, false}};
     for (const B& bn : bins) {
       auto r = count_range(dkeys, bn.lo, bn.hi);
       const int64_t nf = r.second - r.first;
@@ -1132,12 +1157,14 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     // slabs (frames whose lower degree < 65536), (slab_t, coop_t] per-CTA
     // u32 slabs, (256, slab_t] and [1, 256] shared-memory hashes.  Frames
     // whose counters may exceed 16 bits go through the u32 hub path.
-    const int64_t slab_t = 4096;
-    const int64_t coop_t = std::max<int64_t>(1 << 17, slab_t);
+    int64_t slab_t = 4096, coop_t = 1 << 17, small_t = 256;
+    if (force.c4_slab) small_t = slab_t = 0, coop_t = INT64_MAX - 1;
+    if (force.c4_coop || force.c4_hub32) small_t = slab_t = coop_t = 0;
+    if (force.c4_smem) small_t = 0, slab_t = 8192;
     auto rh = count_range(wkeys, coop_t + 1, INT64_MAX);
     auto rl = count_range(wkeys, slab_t + 1, coop_t);
-    auto rs1 = count_range(wkeys, 257, slab_t);
-    auto rs0 = count_range(wkeys, 1, 256);
+    auto rs1 = count_range(wkeys, small_t + 1, slab_t);
+    auto rs0 = count_range(wkeys, 1, small_t);
     const int64_t slab_stride = (n + 31) & ~int64_t(31);
     const int64_t nh = rh.second - rh.first;
     int64_t n_u32_hubs = 0;
@@ -1156,7 +1183,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       std::vector<int64_t> w16, w32;
       for (int64_t h = 0; h < nh; h++) {
         const int sf = hf[h];
-        if (hos[sf] - hrp[sf] < 65536) {
+        if (hos[sf] - hrp[sf] < 65536 && !force.c4_hub32) {
           f16.push_back(sf);
           w16.push_back(wkeys[rh.first + h]);
         } else {
@@ -1255,8 +1282,10 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     }
     const int64_t ns1 = rs1.second - rs1.first;
     if (ns1 > 0) {
-      const int hcap = 2 * (int)slab_t;
+      int hcap = 512;
+      while (hcap < 2 * wkeys[rs1.first]) hcap <<= 1;
       const size_t sm = (size_t)hcap * 8;
+      if (sm > 200 * 1024) throw Error(GD_EINVAL, "forced smem path: frame too large");
       GD_CUDA(cudaFuncSetAttribute(k_c4_frames_smem<256>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       const int grid = (int)std::min<int64_t>(ns1, (int64_t)num_sms() * 8);

@@ -182,3 +182,50 @@ if __name__ == "__main__":
         make_configs("--c2" in sys.argv)
     if "--batch" in sys.argv or len(sys.argv) == 1:
         make_batch()
+
+
+def make_graph_build():
+    """Reference Graph.from_edges / Graph(n, edges) arrays on raw inputs with
+    loops, duplicates, reciprocal pairs, sparse 64-bit and negative ids."""
+    rng = np.random.default_rng(1234)
+    cases = []
+    cases.append(("spec_example", [[1, 2], [2, 1], [2, 2], [1, 3]], {}))
+    big = rng.integers(-(1 << 62), 1 << 62, size=40)
+    cases.append(("sparse64", big[rng.integers(0, 40, size=(300, 2))].tolist(), {}))
+    cases.append(("negative_remap", [[-5, 3], [3, -5], [-5, -5], [7, 3], [-100, 7]], {}))
+    cases.append(("declared_isolated", rng.integers(0, 30, size=(80, 2)).tolist(),
+                  {"num_vertices": 50}))
+    cases.append(("max_id", rng.integers(0, 30, size=(80, 2)).tolist(), {"use_max_id": True}))
+    cases.append(("only_loops", [[3, 3], [4, 4]], {}))
+    cases.append(("dups_heavy", rng.integers(0, 12, size=(500, 2)).tolist(), {}))
+    out = []
+    for name, pairs, opts in cases:
+        g = R.Graph.from_edges(np.asarray(pairs, dtype=np.int64).reshape(-1, 2),
+                               R.ParseOptions(**opts))
+        out.append({"name": name, "pairs": [[int(a), int(b)] for a, b in pairs], "opts": opts,
+                    "n": g.n, "m": g.m, "edges": g.edges.tolist(), "indptr": g.indptr.tolist(),
+                    "indices": g.indices.tolist(), "edge_slot_ids": g.edge_slot_ids.tolist(),
+                    "degrees": g.degrees.tolist(), "orig_ids": [str(x) for x in g.orig_ids]})
+    errors = []
+    for name, pairs, opts in (("declared_out_of_range", [[0, 5]], {"num_vertices": 5}),
+                              ("declared_negative", [[-1, 2]], {"num_vertices": 5}),
+                              ("max_id_negative", [[-1, 2]], {"use_max_id": True})):
+        try:
+            R.Graph.from_edges(np.asarray(pairs, dtype=np.int64), R.ParseOptions(**opts))
+            errors.append({"name": name, "pairs": pairs, "opts": opts, "error": None})
+        except Exception as exc:  # noqa: BLE001
+            errors.append({"name": name, "pairs": pairs, "opts": opts,
+                           "error": type(exc).__name__})
+    for name, n, edges in (("init_loop", 4, [[1, 1]]), ("init_dup", 4, [[0, 1], [1, 0]]),
+                           ("init_range", 4, [[0, 4]])):
+        try:
+            R.Graph(n, np.asarray(edges, dtype=np.int64))
+            errors.append({"name": name, "n": n, "edges": edges, "error": None})
+        except Exception as exc:  # noqa: BLE001
+            errors.append({"name": name, "n": n, "edges": edges, "error": type(exc).__name__})
+    (HERE / "graph_build.json").write_text(json.dumps({"cases": out, "errors": errors}))
+    print("graph build cases:", len(out), "errors:", len(errors))
+
+
+if __name__ == "__main__" and "--graphs" in sys.argv:
+    make_graph_build()

@@ -1,0 +1,199 @@
+"""Parity of the B200 path against the reference's golden vectors and the
+oracle.  Bit-exact everywhere (integer counts)."""
+
+import os
+import subprocess
+import sys
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+
+import paper_1506_04322_b200 as gd
+from helpers import GOLDEN, configs, int_counts, sha, small_graphs
+from oracle import oracle as O
+from paper_1506_04322_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def test_small_graphs_drop_in():
+    for name, n, edges, counts, micro in small_graphs():
+        g = gd.Graph(n, edges)
+        f = gd.graphlet_census(g)
+        assert f.counts == counts, name
+        f.validate()
+        tab = gd.micro_table(g)
+        assert tab.dtype == np.int64 and tab.shape == (len(edges), 10)
+        assert np.array_equal(np.asarray(tab), micro), name
+        if len(edges):
+            assert gd.frequencies_from_micro(g, tab) == f, name
+
+
+def test_foreign_graph_objects_are_accepted():
+    name, n, edges, counts, micro = small_graphs()[-1]
+    foreign = SimpleNamespace(n=n, m=len(edges), edges=edges)
+    assert gd.graphlet_census(foreign).counts == counts
+    assert np.array_equal(np.asarray(gd.micro_table(foreign)), micro)
+    # ParallelConfig is accepted and ignored for results
+    cfg = gd.ParallelConfig(workers=3, batch_size=7, ordering="degree-desc")
+    assert gd.graphlet_census(foreign, cfg).counts == counts
+
+
+def test_edge_order_invariance():
+    name, n, edges, counts, micro = small_graphs()[-1]
+    perm = np.random.default_rng(5).permutation(len(edges))
+    flipped = edges[perm][:, ::-1].copy()
+    g = gd.Graph(n, flipped)
+    assert gd.graphlet_census(g).counts == counts
+    assert np.array_equal(np.asarray(gd.micro_table(g)), micro)
+
+
+def test_degenerate_graphs():
+    for n in (0, 1, 2, 3, 7):
+        g = gd.Graph(n, np.zeros((0, 2), dtype=np.int64))
+        f = gd.graphlet_census(g)
+        f.validate()
+        assert gd.micro_table(g).shape == (0, 10)
+    g = gd.Graph(2, np.asarray([[0, 1]]))
+    assert gd.graphlet_census(g).counts["g2_1"] == 1
+    assert np.array_equal(np.asarray(gd.micro_table(g)), np.zeros((1, 10), dtype=np.int64))
+
+
+FORCED = ["tri_gmem", "tri_small", "c4_slab", "c4_coop", "c4_hub32", "c4_smem",
+          "tri_gmem,c4_coop", "tri_small,c4_hub32"]
+
+
+def _dense_cases():
+    out = []
+    for n, p, seed in ((40, 0.9, 1), (120, 0.5, 2), (300, 0.3, 3), (60, 1.0, 0)):
+        rng = np.random.default_rng(seed)
+        iu = np.triu_indices(n, 1)
+        mask = rng.random(len(iu[0])) < p
+        out.append((f"gnp({n},{p})", n, np.stack([iu[0][mask], iu[1][mask]], 1)))
+    raw = W.chung_lu(3000, 2.1, 8.0, 400.0, seed=11)
+    out.append(("chung_lu3000", raw.n, O.canonical_edges(raw.pairs)))
+    raw = W.rmat(11, 12, 0.57, 0.19, 0.19, seed=3)
+    out.append(("rmat11", raw.n, O.canonical_edges(raw.pairs)))
+    return out
+
+
+@pytest.mark.parametrize("force", FORCED)
+def test_forced_kernel_paths_match_oracle(force):
+    """Every kernel variant (bins) checked against the oracle in a subprocess
+    with GD_FORCE_PATH set (the schedule never changes results)."""
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import paper_1506_04322_b200 as gd
+from oracle import oracle as O
+import test_gpu_parity as T
+for name, n, edges in T._dense_cases():
+    g = gd.Graph(n, edges)
+    f = gd.graphlet_census(g)
+    tab, f2 = gd.micro_census_table(g)
+    want = O.census(edges, n)
+    assert f.counts == want, (name, "global")
+    assert f2 == f, (name, "per-edge sums")
+    rows = O.micro_rows(edges, n)
+    assert np.array_equal(np.asarray(tab), rows), (name, "micro")
+print("ok")
+''' % (str(GOLDEN.parent.parent), str(GOLDEN.parent))
+    env = dict(os.environ, GD_FORCE_PATH=force)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_default_paths_dense_cases():
+    for name, n, edges in _dense_cases():
+        g = gd.Graph(n, edges)
+        tab, f = gd.micro_census_table(g)
+        assert f.counts == O.census(edges, n), name
+        assert np.array_equal(np.asarray(tab), O.micro_rows(edges, n)), name
+        assert gd.graphlet_census(g) == f
+
+
+def test_config1_exact():
+    c = configs()["c1_er"]
+    raw = W.config_graph("c1_er")
+    g = gd.Graph.from_edges(raw.pairs, _declared_n=raw.n)
+    assert sha(np.asarray(g.edges)) == c["edges_sha256"]
+    f = gd.graphlet_census(g)
+    assert f.counts == int_counts(c["counts"])
+    tab = np.asarray(gd.micro_table(g))
+    assert np.array_equal(tab, np.load(GOLDEN / "c1.npz")["micro"])
+    assert sha(tab) == c["micro_sha256"]
+
+
+def test_config2_against_reference():
+    c = configs().get("c2_chung_lu")
+    raw = W.config_graph("c2_chung_lu")
+    g = gd.Graph.from_edges(raw.pairs, _declared_n=raw.n)
+    tab, f = gd.micro_census_table(g)
+    assert gd.graphlet_census(g) == f
+    edges = np.asarray(g.edges)
+    if c is None:
+        assert f.counts == O.census(edges, raw.n)
+    else:
+        assert sha(edges) == c["edges_sha256"]
+        assert f.counts == int_counts(c["counts"])
+        assert sha(np.asarray(tab)) == c["micro_sha256"]
+        idx = np.asarray(c["sample_idx"])
+        assert np.array_equal(np.asarray(tab)[idx], np.asarray(c["sample_rows"]))
+    idx = np.random.default_rng(1).choice(g.m, 3000, replace=False)
+    assert np.array_equal(np.asarray(tab)[idx], O.micro_rows(edges, g.n, idx))
+
+
+def test_config4_batch_feature_matrix():
+    gold = np.load(GOLDEN / "c4_batch.npz")
+    raws = W.config_batch()
+    batch = gd.GraphBatch([r.pairs for r in raws], [r.n for r in raws])
+    assert np.array_equal(batch.m_per_graph, gold["m"])
+    fm = gd.feature_matrix(batch)
+    assert fm.rows.shape == (4096, 17) and not fm.skipped
+    assert np.array_equal(fm.rows, gold["counts"].astype(np.float64))
+    # log/normalise rows equal the reference float math bit for bit
+    fm2 = gd.feature_matrix(batch, log_scale=True, normalize=True)
+    import math
+    row = [math.log1p(float(v)) for v in gold["counts"][0]]
+    tot = sum(row)
+    assert fm2.rows[0].tolist() == [v / tot for v in row]
+    # the plugin seam (census_fn) path gives the same rows
+    some = [gd.Graph.from_edges(r.pairs, _declared_n=r.n) for r in raws[:16]]
+    fm3 = gd.feature_matrix(some, census_fn=gd.graphlet_census)
+    assert np.array_equal(fm3.rows, gold["counts"][:16].astype(np.float64))
+
+
+def _big_parity(name, sample):
+    raw = W.config_graph(name)
+    g = gd.Graph.from_edges(raw.pairs, _declared_n=raw.n)
+    f = gd.graphlet_census(g)
+    tab, f2 = gd.micro_census_table(g)
+    assert f2 == f  # two device routes (global closure vs per-edge sums)
+    assert gd.frequencies_from_micro(g, tab) == f  # dual route over the table
+    f.validate()
+    edges = np.asarray(g.edges)
+    rng = np.random.default_rng(2024)
+    idx = rng.choice(g.m, sample, replace=False)
+    # plus the heaviest edges (largest max-endpoint degree)
+    deg = np.asarray(g.degrees)
+    heavy = np.argsort(-np.maximum(deg[edges[:, 0]], deg[edges[:, 1]]), kind="stable")[:64]
+    idx = np.unique(np.concatenate([idx, heavy]))
+    assert np.array_equal(np.asarray(tab)[idx], O.micro_rows(edges, g.n, idx))
+    gold = configs().get(name)
+    if gold and "counts" in gold:
+        assert f.counts == int_counts(gold["counts"])
+    return g, f
+
+
+def test_config3_rmat20_full_size():
+    g, f = _big_parity("c3_rmat20", 400)
+    assert g.m == 15702776
+    assert f.counts["g3_1"] == 423856269 and f.counts["g4_1"] == 17041022655
+
+
+@pytest.mark.slow
+def test_config5_chung_lu_4m_full_size():
+    g, f = _big_parity("c5_chung_lu_4m", 100)
+    assert g.n == 4_000_000

@@ -1,0 +1,121 @@
+"""Host-side logic of the drop-in: closures, result type, config, classes,
+C-ABI library surface.  CPU only (no device calls)."""
+
+import re
+from math import comb
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_1506_04322_b200 as gd
+from paper_1506_04322_b200 import _native as N
+from paper_1506_04322_b200.census import CensusSums, frequencies_from_sums
+from helpers import small_graphs
+from oracle import oracle as O
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def test_close_triads_hand_cases():
+    # test_census.py:182-191 analogues
+    assert gd.close_triads(3, 0, 0, 3) == {"g3_1": 1, "g3_2": 0, "g3_3": 0, "g3_4": 0}
+    assert gd.close_triads(0, 4, 2, 4) == {"g3_1": 0, "g3_2": 2, "g3_3": 2, "g3_4": 0}
+    with pytest.raises(gd.ConsistencyError):
+        gd.close_triads(4, 0, 0, 5)
+    with pytest.raises(gd.ConsistencyError):
+        gd.close_triads(0, 3, 0, 5)
+
+
+def test_close_quads_hand_cases():
+    f = gd.close_quads(CensusSums(n_tt=1, n_ts=4, outside=4), n=4, m=5)
+    assert f["g4_2"] == 1 and sum(f.values()) == 1
+    f = gd.close_quads(CensusSums(cycle4=4, n_susv=4, outside=4), n=4, m=4)
+    assert f["g4_4"] == 1 and f["g4_6"] == 0 and sum(f.values()) == 1
+    with pytest.raises(gd.ConsistencyError):
+        gd.close_quads(CensusSums(clique4=5), n=5, m=6)
+    with pytest.raises(gd.ConsistencyError):
+        gd.close_quads(CensusSums(cycle4=4, n_susv=2), n=5, m=4)
+
+
+def test_closures_match_reference_on_golden_sums():
+    for name, n, edges, counts, micro in small_graphs():
+        sums = O.sums_from_rows(micro, n, len(edges))
+        f = frequencies_from_sums(CensusSums.from_tuple(sums), n, len(edges))
+        assert f.counts == counts, name
+
+
+def test_beyond_64_bits_exact():
+    n = 200_000
+    f = frequencies_from_sums(CensusSums(), n, 0)
+    assert f.counts["g4_11"] == comb(n, 4) > 2 ** 63
+    f.validate()
+
+
+def test_frequencies_validate_and_eq():
+    f = frequencies_from_sums(CensusSums(), 5, 0)
+    g = gd.GraphletFrequencies(counts=dict(f.counts), n=5, m=0)
+    assert f == g
+    bad = dict(f.counts)
+    bad["g2_1"] = 1
+    with pytest.raises(gd.ConsistencyError):
+        gd.GraphletFrequencies(counts=bad, n=5, m=0).validate()
+    with pytest.raises(ValueError):
+        gd.GraphletFrequencies(counts={"g2_1": 0}, n=1, m=0)
+
+
+def test_parallel_config_validation():
+    gd.ParallelConfig(workers=4, batch_size=1, ordering="degree-desc")
+    for kw in ({"workers": 0}, {"batch_size": 0}, {"batch_size": 4097}, {"ordering": "x"}):
+        with pytest.raises(ValueError):
+            gd.ParallelConfig(**kw)
+
+
+def test_classes():
+    assert len(gd.CLASS_IDS) == 17 and gd.CLASS_IDS[0] == "g2_1" and gd.CLASS_IDS[-1] == "g4_11"
+    assert gd.classes_for(4, connected_only=True) == ("g4_1", "g4_2", "g4_3", "g4_4", "g4_5", "g4_6")
+    for c in gd.CLASS_IDS:
+        assert gd.complement_class(gd.complement_class(c)) == c
+
+
+def test_gfd_host_math():
+    name, n, edges, counts, _ = small_graphs()[-1]
+    f = gd.GraphletFrequencies(counts=counts, n=n, m=len(edges))
+    v = gd.gfd(f, 4, "all")
+    assert abs(sum(v.values) - 1.0) < 1e-12
+
+
+def _header_symbols():
+    text = (ROOT / "include" / "gd_api.h").read_text()
+    return sorted(set(re.findall(r"GD_API[^;]*?\b(gd_[a-z0-9_]+)\s*\(", text, re.S)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = N.load_library()
+    declared = _header_symbols()
+    assert len(declared) >= 15
+    bound = {name for name, _, _ in N.SIGNATURES}
+    assert set(declared) == bound
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.gd_version() == 1
+
+
+def test_no_cpu_fallback_without_device():
+    lib = N.load_library()
+    if lib.gd_device_ok():
+        pytest.skip("a device is present")
+    with pytest.raises(gd.DeviceError):
+        gd.Graph(3, np.asarray([[0, 1], [1, 2]]))
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    with pytest.raises(gd.DeviceError):
+        N.load_library(tmp_path / "libgdgpu.so")
+
+
+def test_product_does_not_import_oracle():
+    pkg = ROOT / "paper_1506_04322_b200"
+    for p in pkg.rglob("*.py"):
+        txt = p.read_text()
+        assert "import oracle" not in txt and "from oracle" not in txt, p
