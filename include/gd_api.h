@@ -146,6 +146,13 @@ GD_API int gd_graph_timings(const gd_graph* g, float* ms, int capacity, const ch
 /* work statistics of the last census call (wedges, triangles, ...) */
 GD_API int gd_graph_stats(const gd_graph* g, int64_t* values, int capacity, const char** names);
 
+/* Select the CUDA device of the calling thread (one process per GPU). */
+GD_API int gd_set_device(int device);
+
+/* Device memory for GD_OUTPUT_DEVICE tables (device-resident runs). */
+GD_API void* gd_device_alloc(int64_t bytes);
+GD_API void  gd_device_free(void* p);
+
 /* Pinned host memory helpers (for end-to-end runs without torch). */
 GD_API void* gd_host_alloc(int64_t bytes);
 GD_API void  gd_host_free(void* p);

@@ -55,6 +55,9 @@ SIGNATURES = (
                                         ctypes.POINTER(ctypes.c_char_p)]),
     ("gd_graph_stats", ctypes.c_int, [_vp, _i64p, ctypes.c_int,
                                       ctypes.POINTER(ctypes.c_char_p)]),
+    ("gd_set_device", ctypes.c_int, [ctypes.c_int]),
+    ("gd_device_alloc", _vp, [ctypes.c_int64]),
+    ("gd_device_free", None, [_vp]),
     ("gd_host_alloc", _vp, [ctypes.c_int64]),
     ("gd_host_free", None, [_vp]),
     ("gd_flush_l2", ctypes.c_int, []),

@@ -148,18 +148,37 @@ def micro_table(g, config: ParallelConfig | None = None, *, pinned: bool = True)
     return table
 
 
-def micro_census_table(g, config: ParallelConfig | None = None, *, pinned: bool = True):
-    """micro_table plus the global frequencies from the same device pass."""
+def micro_census_table(g, config: ParallelConfig | None = None, *, pinned: bool = True,
+                       out: np.ndarray | None = None, device_out: int | None = None):
+    """micro_table plus the global frequencies from the same device pass.
+
+    ``out``: a C-contiguous int64 (m, 10) host array to fill (e.g. a reused
+    pinned buffer); ``device_out``: a device pointer (int) of m*10 int64 to
+    leave the table in HBM (then the returned table is None)."""
     _check_config(config)
     n, m = int(g.n), int(g.m)
     if m == 0:
         return np.zeros((0, len(RAW_MICRO_FIELDS)), dtype=np.int64), \
             frequencies_from_sums(CensusSums(), n, m)
     dg = _device(g)
-    table = N.pinned_empty((m, N.NUM_MICRO)) if pinned else np.empty((m, N.NUM_MICRO), np.int64)
+    flags = 0
+    if device_out is not None:
+        table = None
+        tptr = ctypes.c_void_p(int(device_out))
+        flags = N.GD_OUTPUT_DEVICE
+    else:
+        if out is not None:
+            if out.shape != (m, N.NUM_MICRO) or out.dtype != np.int64 or \
+                    not out.flags["C_CONTIGUOUS"]:
+                raise ValueError("out must be a C-contiguous int64 (m, 10) array")
+            table = out
+        else:
+            table = N.pinned_empty((m, N.NUM_MICRO)) if pinned else \
+                np.empty((m, N.NUM_MICRO), np.int64)
+        tptr = N.vptr(table)
     sums = np.zeros(2 * N.NUM_SUMS, dtype=np.uint64)
     seen = np.zeros(1, dtype=np.int64)
-    N.check(N.lib().gd_census_per_edge(dg.handle, N.vptr(table), 0,
+    N.check(N.lib().gd_census_per_edge(dg.handle, tptr, flags,
                                        N.ptr(sums, ctypes.c_uint64), N.ptr(seen)))
     if int(seen[0]) != m:
         raise ConsistencyError(f"processed {int(seen[0])} edges, expected {m}")

@@ -17,6 +17,7 @@ struct gd_graph {
 namespace gd {
 
 static thread_local std::string t_last_error;
+thread_local long long g_launches = 0;
 
 int num_sms() {
   static int sms = 0;
@@ -325,6 +326,24 @@ int gd_graph_stats(const gd_graph* h, int64_t* values, int capacity, const char*
   for (int i = 0; i < k; i++) values[i] = h->stats[i];
   if (names) *names = h->stats_names.c_str();
   return k;
+}
+
+int gd_set_device(int device) {
+  return guarded([&] { GD_CUDA(cudaSetDevice(device)); });
+}
+
+void* gd_device_alloc(int64_t bytes) {
+  void* p = nullptr;
+  if (bytes <= 0) return nullptr;
+  if (cudaMalloc(&p, (size_t)bytes) != cudaSuccess) {
+    t_last_error = "cudaMalloc failed";
+    return nullptr;
+  }
+  return p;
+}
+
+void gd_device_free(void* p) {
+  if (p) cudaFree(p);
 }
 
 void* gd_host_alloc(int64_t bytes) {

@@ -32,8 +32,13 @@ struct Error : std::runtime_error {
                                       cudaGetErrorString(_e));               \
   } while (0)
 
+// Every launch of one of our kernels goes through GD_LAUNCH_CHECK, which
+// also counts it (reported as the "launches" statistic of a census).
+extern thread_local long long g_launches;
+
 #define GD_LAUNCH_CHECK(what)                                                \
   do {                                                                       \
+    ::gd::g_launches++;                                                      \
     cudaError_t _e = cudaGetLastError();                                     \
     if (_e != cudaSuccess)                                                   \
       throw ::gd::Error(GD_ECUDA, std::string("launch ") + (what) + ": " +   \

@@ -1018,6 +1018,7 @@ static ForcePaths read_force() {
 void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long long* sums_dev,
                 unsigned long long* seen_dev, CensusExtras& ex, cudaStream_t s) {
   const ForcePaths force = read_force();
+  const long long launches0 = g_launches;
   const int64_t n = g.n, m = g.m, G = g.G;
   const View v = make_view(g);
   Timer timer(s);
@@ -1343,6 +1344,8 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   GD_CUDA(cudaMemcpyAsync(hk4.data(), k4tot.p, 2 * G * 8, cudaMemcpyDeviceToHost, s));
   GD_CUDA(cudaMemcpyAsync(hc4.data(), c4tot2.p, 2 * G * 8, cudaMemcpyDeviceToHost, s));
   timer.collect(ex.ms, ex.names);
+  ex.stats.push_back(g_launches - launches0);
+  ex.stats_names.push_back("launches");
   for (int64_t i = 0; i < G; i++) {
     ex.k4tot[i] = ((unsigned __int128)hk4[2 * i + 1] << 64) | hk4[2 * i];
     ex.c4tot2[i] = ((unsigned __int128)hc4[2 * i + 1] << 64) | hc4[2 * i];
