@@ -211,6 +211,19 @@ __global__ void k_osplit(const int64_t* __restrict__ rp, const int32_t* __restri
     osplit[r] = lower_bound_dev(col, rp[r], rp[r + 1], (int32_t)(r + 1));
 }
 
+// e2o / e2i: the two slots of every edge (warp per row)
+__global__ void k_edge_slots(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                             const int32_t* __restrict__ seid, int64_t n,
+                             int64_t* __restrict__ e2o, int64_t* __restrict__ e2i) {
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
+    for (int64_t q = rp[r] + (threadIdx.x & 31); q < rp[r + 1]; q += 32) {
+      const int e = seid[q];
+      if (col[q] > r) e2o[e] = q; else e2i[e] = q;
+    }
+  }
+}
+
 __global__ void k_vgraph(const int32_t* __restrict__ r2d, int64_t n,
                          const int64_t* __restrict__ voff, int64_t G,
                          int32_t* __restrict__ vgraph) {
@@ -379,9 +392,16 @@ void finish_graph(DevGraph& g, DBuf<unsigned long long>& ukeys, int64_t m, int64
     k_slot_cols<<<grid_for(2 * m), 256, 0, s>>>(sk2.p, 2 * m, g.col.p);
     GD_LAUNCH_CHECK("slot_cols");
   }
+  g.e2o.alloc(m, s);
+  g.e2i.alloc(m, s);
   if (n) {
     k_osplit<<<grid_for(n), 256, 0, s>>>(g.rp.p, g.col.p, n, g.osplit.p);
     GD_LAUNCH_CHECK("osplit");
+    if (m) {
+      k_edge_slots<<<grid_for(n * 32), 256, 0, s>>>(g.rp.p, g.col.p, g.seid.p, n, g.e2o.p,
+                                                   g.e2i.p);
+      GD_LAUNCH_CHECK("edge_slots");
+    }
   }
   GD_CUDA(cudaStreamSynchronize(s));
   if (g.max_deg >= (1 << 24) - 1)

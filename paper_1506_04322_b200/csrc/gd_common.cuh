@@ -110,6 +110,8 @@ struct DevGraph {
   DBuf<int32_t> col;    // [2m] neighbour rank ids, rows strictly ascending
   DBuf<int32_t> seid;   // [2m] canonical edge id of each slot
   DBuf<int64_t> osplit; // [n] absolute slot index of the first neighbour > row
+  DBuf<int64_t> e2o;    // [m] slot of edge e in the row of its lower-rank endpoint
+  DBuf<int64_t> e2i;    // [m] slot of edge e in the row of its higher-rank endpoint
   DBuf<int32_t> deg;    // [n] degree by rank id
   DBuf<int32_t> r2d;    // [n] rank id -> dense id
   DBuf<int32_t> d2r;    // [n] dense id -> rank id
