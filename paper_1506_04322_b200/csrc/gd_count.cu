@@ -64,26 +64,28 @@ typedef unsigned __int128 u128;
 
 // ------------------------------------------------------------------------
 // Per-frame scratch layout (shared memory for bounded frames, a global slab
-// per CTA for the largest ones).  Bitmap rows use an odd word stride so the
-// rows of different local vertices fall in different banks.
+// per CTA for the largest ones).  Bitmap rows are 64-bit words with an odd
+// row stride (conflict-free across rows).
 // ------------------------------------------------------------------------
 struct FrameLayout {
-  int cap;   // max frame size D
-  int hcap;  // hash capacity (pow2 >= 2*cap)
-  int rows;  // 1: pass-A bitmap rows
-  int accum; // 1: pass-B accumulators
-  size_t o_lv, o_p, o_hk, o_hv, o_rows, o_tri2, o_tl, o_dl, o_acc;
+  int cap;     // max frame size D
+  int hcap;    // hash capacity (pow2 >= 2*cap)
+  int hitcap;  // local-edge (hit) list capacity, 0 = none
+  int rows;    // 1: pass-A bitmap rows
+  int accum;   // 1: pass-B accumulators
+  size_t o_qb, o_lv, o_p, o_hk, o_hv, o_rows, o_tri2, o_hits, o_tl, o_dl, o_acc;
   size_t bytes;
 };
 
-__host__ __device__ __forceinline__ int row_stride(int W) { return W | 1; }
+__host__ __device__ __forceinline__ int row_stride64(int W) { return W | 1; }
 
-FrameLayout make_layout(int cap, bool rows, bool accum) {
+FrameLayout make_layout(int cap, bool rows, bool accum, int hitcap) {
   FrameLayout L{};
   L.cap = cap;
   int h = 32;
   while (h < 2 * cap) h <<= 1;
   L.hcap = h;
+  L.hitcap = rows ? hitcap : 0;
   L.rows = rows;
   L.accum = accum;
   size_t o = 0;
@@ -92,78 +94,99 @@ FrameLayout make_layout(int cap, bool rows, bool accum) {
     o += (b + 15) & ~size_t(15);
     return r;
   };
+  L.o_qb = take(8 * (size_t)cap);
   if (accum) L.o_acc = take(sizeof(u64) * 3 * cap);
-  L.o_lv = take(4 * cap);
-  L.o_p = take(4 * (cap + 1));
-  L.o_hk = take(4 * h);
-  L.o_hv = take(4 * h);
   if (rows) {
-    const int W = (cap + 31) / 32;
-    L.o_rows = take(4ull * cap * row_stride(W));
-    L.o_tri2 = take(4 * cap);
+    const int W = (cap + 63) / 64;
+    L.o_rows = take(8ull * cap * row_stride64(W));
   }
+  if (L.hitcap) L.o_hits = take(8ull * L.hitcap);
+  L.o_lv = take(4 * (size_t)cap);
+  L.o_p = take(4 * (size_t)(cap + 1));
+  L.o_hk = take(4 * (size_t)h);
+  L.o_hv = take(4 * (size_t)h);
+  if (rows) L.o_tri2 = take(4 * (size_t)cap);
   if (accum) {
-    L.o_tl = take(4 * cap);
-    L.o_dl = take(4 * cap);
+    L.o_tl = take(4 * (size_t)cap);
+    L.o_dl = take(4 * (size_t)cap);
   }
   L.bytes = o;
   return L;
 }
 
-__device__ __forceinline__ void hash_insert(int* hk, int* hv, int hmask, int key, int val) {
-  unsigned h = hash32((unsigned)key) & hmask;
-  while (true) {
-    int old = atomicCAS(&hk[h], -1, key);
-    if (old == -1 || old == key) {
-      hv[h] = val;
-      return;
+// Multiplicative hashing into a power-of-two table (top bits), linear probing.
+__device__ __forceinline__ unsigned mhash(unsigned x, int shift) {
+  return (x * 2654435761u) >> shift;
+}
+
+struct LocalHash {
+  int* hk;
+  int* hv;
+  int hmask, hshift;
+  __device__ __forceinline__ void insert(int key, int val) const {
+    unsigned h = mhash((unsigned)key, hshift);
+    while (true) {
+      const int old = atomicCAS(&hk[h], -1, key);
+      if (old == -1 || old == key) {
+        hv[h] = val;
+        return;
+      }
+      h = (h + 1) & hmask;
     }
-    h = (h + 1) & hmask;
   }
-}
-
-__device__ __forceinline__ int hash_find(const int* hk, const int* hv, int hmask, int key) {
-  unsigned h = hash32((unsigned)key) & hmask;
-  while (true) {
+  __device__ __forceinline__ int find(int key) const {
+    unsigned h = mhash((unsigned)key, hshift);
     int k = hk[h];
-    if (k == key) return hv[h];
-    if (k == -1) return -1;
-    h = (h + 1) & hmask;
+    while (k != key) {
+      if (k == -1) return -1;
+      h = (h + 1) & hmask;
+      k = hk[h];
+    }
+    return hv[h];
   }
-}
+};
 
-// Load N+(a) into Lv, the item prefix P (from the global out-item prefix OP)
-// and the hash of Lv.  Returns D; total items in P[D].
+// Load N+(a) into Lv, QB[j] = osplit[x_j] - P[j] (so item i of segment j
+// lives at slot QB[j] + i), the item prefix P (from the global out-item
+// prefix OP) and the hash of Lv.  Returns D; total items in P[D].
 template <int NT>
 __device__ int frame_load(const View& g, int a, char* mem, const FrameLayout& L,
-                          const int64_t* __restrict__ OP, int& hmask) {
+                          const int64_t* __restrict__ OP, LocalHash& H) {
   const int64_t base = g.osplit[a];
   const int D = (int)(g.rp[a + 1] - base);
   int* Lv = (int*)(mem + L.o_lv);
   int* P = (int*)(mem + L.o_p);
-  int* hk = (int*)(mem + L.o_hk);
-  int* hv = (int*)(mem + L.o_hv);
-  int H = pow2_at_least(2 * D);
-  if (H > L.hcap) H = L.hcap;
-  hmask = H - 1;
+  int64_t* QB = (int64_t*)(mem + L.o_qb);
+  int hsize = pow2_at_least(2 * D);
+  if (hsize > L.hcap) hsize = L.hcap;
+  H.hk = (int*)(mem + L.o_hk);
+  H.hv = (int*)(mem + L.o_hv);
+  H.hmask = hsize - 1;
+  H.hshift = 32 - (31 - __clz(hsize));
   const int64_t p0 = OP[base];
   for (int j = threadIdx.x; j < D; j += NT) {
-    Lv[j] = g.col[base + j];
-    P[j] = (int)(OP[base + j] - p0);
+    const int x = g.col[base + j];
+    const int pj = (int)(OP[base + j] - p0);
+    Lv[j] = x;
+    P[j] = pj;
+    QB[j] = g.osplit[x] - pj;
   }
   if (threadIdx.x == 0) P[D] = (int)(OP[base + D] - p0);
-  for (int h = threadIdx.x; h < H; h += NT) hk[h] = -1;
+  for (int h = threadIdx.x; h < hsize; h += NT) H.hk[h] = -1;
   __syncthreads();
-  for (int j = threadIdx.x; j < D; j += NT) hash_insert(hk, hv, hmask, Lv[j], j);
+  for (int j = threadIdx.x; j < D; j += NT) H.insert(Lv[j], j);
   return D;
 }
 
-// Items [0, total) of a frame, item i -> (j, pos) with P[j] <= i < P[j+1]:
+// Items [0, total) of a frame, item i -> segment j with P[j] <= i < P[j+1]:
 // warp chunks of 32*K items, lane-interleaved (consecutive lanes read
-// consecutive entries of one row), one binary search per lane per chunk.
+// consecutive entries of one row), one binary search per lane per chunk, and
+// U items per lane in flight (their col[] loads are issued back to back).
+// f(j, i, q, y) receives the slot q = QB[j] + i and the neighbour y = col[q].
 template <int NT, typename F>
-__device__ __forceinline__ void for_frame_items(const int* P, int D, int total, F&& f) {
-  constexpr int K = 8;
+__device__ __forceinline__ void for_frame_items(const View& g, const int* P, const int64_t* QB,
+                                                int D, int total, F&& f) {
+  constexpr int K = 8, U = 1;
   constexpr int NW = NT / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int c0 = warp * 32 * K; c0 < total; c0 += NW * 32 * K) {
@@ -171,16 +194,32 @@ __device__ __forceinline__ void for_frame_items(const int* P, int D, int total, 
     int i = c0 + lane;
     if (i >= c1) continue;
     int j = find_segment(P, D, i);
-    int pj = P[j], pj1 = P[j + 1];
-    for (; i < c1; i += 32) {
-      while (pj1 <= i) {
-        ++j;
-        pj = pj1;
-        pj1 = P[j + 1];
+    int pj1 = P[j + 1];
+    for (; i < c1; i += 32 * U) {
+      int jj[U];
+      int64_t qq[U];
+      int yy[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int ii = i + 32 * u;
+        if (ii < c1) {
+          while (pj1 <= ii) pj1 = P[++j + 1];
+          jj[u] = j;
+          qq[u] = QB[j] + ii;
+        }
       }
-      f(j, i - pj);
+#pragma unroll
+      for (int u = 0; u < U; u++)
+        if (i + 32 * u < c1) yy[u] = __ldg(g.col + qq[u]);
+#pragma unroll
+      for (int u = 0; u < U; u++)
+        if (i + 32 * u < c1) f(jj[u], i + 32 * u, qq[u], yy[u]);
     }
   }
+}
+
+__device__ __forceinline__ u64 pack_hit(int j, int k, int i) {
+  return ((u64)(unsigned)j << 48) | ((u64)(unsigned)k << 32) | (u64)(unsigned)i;
 }
 
 // ------------------------------------------------------------------------
@@ -190,54 +229,73 @@ template <int NT>
 __device__ void tri_frame(const View& g, int a, char* mem, const FrameLayout& L,
                           const int64_t* __restrict__ OP, u64* __restrict__ tcs,
                           u64* __restrict__ vT, u64* __restrict__ k4tot) {
-  int hmask;
-  const int D = frame_load<NT>(g, a, mem, L, OP, hmask);
+  __shared__ int nhits;
+  LocalHash H;
+  const int D = frame_load<NT>(g, a, mem, L, OP, H);
   const int* Lv = (const int*)(mem + L.o_lv);
   const int* P = (const int*)(mem + L.o_p);
-  const int* hk = (const int*)(mem + L.o_hk);
-  const int* hv = (const int*)(mem + L.o_hv);
-  unsigned* rows = (unsigned*)(mem + L.o_rows);
+  const int64_t* QB = (const int64_t*)(mem + L.o_qb);
+  u64* rows = (u64*)(mem + L.o_rows);
   unsigned* tri2 = (unsigned*)(mem + L.o_tri2);
-  const int W = (D + 31) >> 5;
-  const int RS = row_stride(W);
-  for (int i = threadIdx.x; i < D * RS; i += NT) rows[i] = 0u;
+  u64* hits = (u64*)(mem + L.o_hits);
+  const int W = (D + 63) >> 6;
+  const int RS = row_stride64(W);
+  for (int i = threadIdx.x; i < D * RS; i += NT) rows[i] = 0ull;
   for (int j = threadIdx.x; j < D; j += NT) tri2[j] = 0u;
+  if (threadIdx.x == 0) nhits = 0;
   __syncthreads();
   const int total = P[D];
-  // sweep 1: local adjacency bitmaps (undirected)
-  for_frame_items<NT>(P, D, total, [&](int j, int pos) {
-    const int y = g.col[g.osplit[Lv[j]] + pos];
-    const int k = hash_find(hk, hv, hmask, y);
+  const int hitcap = (D < 65536) ? L.hitcap : 0;
+  // sweep 1: local adjacency bitmaps (undirected) + the list of local edges
+  for_frame_items<NT>(g, P, QB, D, total, [&](int j, int i, int64_t, int y) {
+    const int k = H.find(y);
     if (k >= 0) {
-      atomicOr(&rows[j * RS + (k >> 5)], 1u << (k & 31));
-      atomicOr(&rows[k * RS + (j >> 5)], 1u << (j & 31));
+      atomicOr(&rows[j * RS + (k >> 6)], 1ull << (k & 63));
+      atomicOr(&rows[k * RS + (j >> 6)], 1ull << (j & 63));
+      if (hitcap) {  // warp-aggregated append
+        const unsigned act = __activemask();
+        const int leader = __ffs(act) - 1;
+        int h0 = 0;
+        if ((int)lane_id() == leader) h0 = atomicAdd(&nhits, __popc(act));
+        const int h = __shfl_sync(act, h0, leader) + __popc(act & ((1u << lane_id()) - 1u));
+        if (h < hitcap) hits[h] = pack_hit(j, k, i);
+      }
     }
   });
   __syncthreads();
   // sweep 2: each local edge (x_j, x_k) is the triangle {a, x_j, x_k}; its
   // common local neighbours are the 4-cliques {a, x_j, x_k, z}
-  for_frame_items<NT>(P, D, total, [&](int j, int pos) {
-    const int64_t q = g.osplit[Lv[j]] + pos;
-    const int k = hash_find(hk, hv, hmask, g.col[q]);
-    if (k >= 0) {
-      unsigned c = 0;
-      const unsigned* rj = rows + j * RS;
-      const unsigned* rk = rows + k * RS;
-      for (int w = 0; w < W; w++) c += __popc(rj[w] & rk[w]);
-      atomicAdd(&tcs[q], (1ull << kTriShift) + c);
-      if (c) {
-        atomicAdd(&tri2[j], c);
-        atomicAdd(&tri2[k], c);
-      }
+  auto local_edge = [&](int j, int k, int64_t q) {
+    unsigned c = 0;
+    const u64* rj = rows + j * RS;
+    const u64* rk = rows + k * RS;
+    for (int w = 0; w < W; w++) c += __popcll(rj[w] & rk[w]);
+    atomicAdd(&tcs[q], (1ull << kTriShift) + c);
+    if (c) {
+      atomicAdd(&tri2[j], c);
+      atomicAdd(&tri2[k], c);
     }
-  });
+  };
+  const int nh = nhits;
+  if (hitcap > 0 && nh <= hitcap) {
+    for (int h = threadIdx.x; h < nh; h += NT) {
+      const u64 e = hits[h];
+      const int j = (int)(e >> 48), k = (int)((e >> 32) & 0xffff), i = (int)(unsigned)e;
+      local_edge(j, k, QB[j] + i);
+    }
+  } else {
+    for_frame_items<NT>(g, P, QB, D, total, [&](int j, int, int64_t q, int y) {
+      const int k = H.find(y);
+      if (k >= 0) local_edge(j, k, q);
+    });
+  }
   __syncthreads();
   const int64_t base = g.osplit[a];
   u64 t2sum = 0, dlsum = 0;
   for (int j = threadIdx.x; j < D; j += NT) {
     unsigned dl = 0;
-    const unsigned* rj = rows + j * RS;
-    for (int w = 0; w < W; w++) dl += __popc(rj[w]);
+    const u64* rj = rows + j * RS;
+    for (int w = 0; w < W; w++) dl += __popcll(rj[w]);
     if (dl) {
       atomicAdd(&tcs[base + j], ((u64)dl << kTriShift) + (tri2[j] >> 1));
       atomicAdd(&vT[Lv[j]], (u64)dl);
@@ -277,12 +335,11 @@ __device__ void trisum_frame(const View& g, int a, char* mem, const FrameLayout&
                              const int64_t* __restrict__ OP, const u64* __restrict__ tcs,
                              u64* __restrict__ tsl, u64* __restrict__ tsh,
                              u64* __restrict__ tsd) {
-  int hmask;
-  const int D = frame_load<NT>(g, a, mem, L, OP, hmask);
+  LocalHash H;
+  const int D = frame_load<NT>(g, a, mem, L, OP, H);
   const int* Lv = (const int*)(mem + L.o_lv);
   const int* P = (const int*)(mem + L.o_p);
-  const int* hk = (const int*)(mem + L.o_hk);
-  const int* hv = (const int*)(mem + L.o_hv);
+  const int64_t* QB = (const int64_t*)(mem + L.o_qb);
   int* tL = (int*)(mem + L.o_tl);
   int* dL = (int*)(mem + L.o_dl);
   u64* acc = (u64*)(mem + L.o_acc);
@@ -297,9 +354,8 @@ __device__ void trisum_frame(const View& g, int a, char* mem, const FrameLayout&
   __syncthreads();
   const int total = P[D];
   const u64 deg_a = (u64)g.deg[a];
-  for_frame_items<NT>(P, D, total, [&](int j, int pos) {
-    const int64_t q = g.osplit[Lv[j]] + pos;
-    const int k = hash_find(hk, hv, hmask, g.col[q]);
+  for_frame_items<NT>(g, P, QB, D, total, [&](int j, int, int64_t q, int y) {
+    const int k = H.find(y);
     if (k < 0) return;
     const u64 t_jk = tcs[q] >> kTriShift;
     // edge (x_j, x_k), lo side x_j, third vertex a
@@ -415,14 +471,14 @@ template <bool C16>
 struct HashCounter {  // shared-memory open-addressing hash, u32 or u16 counts
   int* hk;
   unsigned* hv;  // C16: two counts per word
-  int hmask;
+  int hmask, hshift;
   __device__ __forceinline__ int slot(int x) const {
-    unsigned h = hash32((unsigned)x) & hmask;
+    unsigned h = mhash((unsigned)x, hshift);
     while (hk[h] != x) h = (h + 1) & hmask;
     return (int)h;
   }
   __device__ __forceinline__ void inc(int x) const {
-    unsigned h = hash32((unsigned)x) & hmask;
+    unsigned h = mhash((unsigned)x, hshift);
     while (true) {
       int old = atomicCAS(&hk[h], -1, x);
       if (old == -1 || old == x) break;
@@ -448,6 +504,7 @@ template <int NT, int MODE, typename C>
 __device__ u64 wedge_sweep(const View& g, const int64_t* __restrict__ WP, int64_t b, int64_t o,
                            int64_t i0, int64_t i1, const C& ctr, bool per_edge,
                            u64* __restrict__ c4s) {
+  constexpr int U = 1;  // items per lane in flight (U > 1 measured slower)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int nw = NT / 32;
   constexpr int64_t CH = 32 * kWedgeK;
@@ -459,40 +516,58 @@ __device__ u64 wedge_sweep(const View& g, const int64_t* __restrict__ WP, int64_
     int64_t p = wedge_slot(WP, b, o, i);
     int64_t wp1 = WP[p + 1];
     int64_t base = g.rp[g.col[p]] - WP[p];  // slot of item i in row w: base + i
-    u64 top = 0;                            // per-edge: pending sum for slot p (edge s-w)
-    for (; i < c1; i += 32) {
-      if (wp1 <= i) {
-        if (MODE == kUse && per_edge && top) {
-          atomicAdd(&c4s[p], top);
-          top = 0;
+    int64_t ptop = p;                       // per-edge: pending sum for slot ptop (edge s-w)
+    u64 top = 0;
+    for (; i < c1; i += 32 * U) {
+      int64_t pp[U], qq[U];
+      int xx[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t ii = i + 32 * u;
+        if (ii < c1) {
+          if (wp1 <= ii) {
+            do {
+              p++;
+              wp1 = WP[p + 1];
+            } while (wp1 <= ii);
+            base = g.rp[g.col[p]] - WP[p];
+          }
+          pp[u] = p;
+          qq[u] = base + ii;
         }
-        do {
-          p++;
-          wp1 = WP[p + 1];
-        } while (wp1 <= i);
-        base = g.rp[g.col[p]] - WP[p];
       }
-      const int64_t q = base + i;
-      const int x = g.col[q];
-      if (MODE == kCount) {
-        ctr.inc(x);
-      } else if (MODE == kZero) {
-        ctr.zero(x);
-      } else if (MODE == kTake) {
-        const u64 c = ctr.take(x);
-        local += c * (c - (c > 0));
-      } else {
-        const u64 c = ctr.get(x) - 1u;
-        if (c) {
-          local += c;
-          if (per_edge) {
-            atomicAdd(&c4s[q], c);  // edge w-x
-            top += c;
+#pragma unroll
+      for (int u = 0; u < U; u++)
+        if (i + 32 * u < c1) xx[u] = __ldg(g.col + qq[u]);
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        if (i + 32 * u >= c1) break;
+        const int x = xx[u];
+        if (MODE == kCount) {
+          ctr.inc(x);
+        } else if (MODE == kZero) {
+          ctr.zero(x);
+        } else if (MODE == kTake) {
+          const u64 c = ctr.take(x);
+          local += c * (c - (c > 0));
+        } else {
+          const u64 c = ctr.get(x) - 1u;
+          if (c) {
+            local += c;
+            if (per_edge) {
+              atomicAdd(&c4s[qq[u]], c);  // edge w-x
+              if (pp[u] != ptop) {
+                if (top) atomicAdd(&c4s[ptop], top);
+                top = 0;
+                ptop = pp[u];
+              }
+              top += c;
+            }
           }
         }
       }
     }
-    if (MODE == kUse && per_edge && top) atomicAdd(&c4s[p], top);
+    if (MODE == kUse && per_edge && top) atomicAdd(&c4s[ptop], top);
   }
   return local;
 }
@@ -515,7 +590,7 @@ k_c4_frames_smem(View g, const int64_t* __restrict__ WP, const int* __restrict__
     const int64_t total = i1 - i0;
     int H = pow2_at_least((int)(2 * total < (int64_t)hcap ? 2 * total : (int64_t)hcap));
     if (H > hcap) H = hcap;
-    HashCounter<C16> ctr{hk, hv, H - 1};
+    HashCounter<C16> ctr{hk, hv, H - 1, 32 - (31 - __clz(H))};
     for (int h = threadIdx.x; h < H; h += NT) hk[h] = -1;
     for (int h = threadIdx.x; h < (C16 ? H / 2 : H); h += NT) hv[h] = 0u;
     __syncthreads();
@@ -1025,6 +1100,8 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   exclusive_scan(witems.p, WP.p, S + 1, s);
   oitems.release();
   witems.release();
+  int64_t tot_items = 0;
+  if (S) GD_CUDA(cudaMemcpyAsync(&tot_items, OP.p + S, 8, cudaMemcpyDeviceToHost, s));
   std::vector<int64_t> dkeys, wkeys;
   std::vector<char> wbig;
   if (n) {
@@ -1041,17 +1118,21 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   // ---- pass A / pass B: triangle frames by D = |N+(a)| ----------------------
   const int64_t maxD = dkeys.empty() ? 0 : dkeys[0];
   auto run_frames = [&](bool trisum) {
-    struct B { int64_t lo, hi; int nt; bool gmem; };
-    std::vector<B> bins = {{1025, INT64_MAX, 512, true}, {513, 1024, 512, false},
-                           {129, 512, 256, false}, {33, 128, 128, false}, {2, 32, 32, false}};
-    if (force.tri_gmem) bins = {{2, INT64_MAX, 512, true}};
-    if (force.tri_small) bins = {{2, INT64_MAX, 32, false}};
+    struct B { int64_t lo, hi; int nt; bool gmem; int hitcap; };
+    std::vector<B> bins = {{1025, INT64_MAX, 512, true, 65536},
+                           {513, 1024, 512, false, 4096},
+                           {129, 512, 256, false, 4096},
+                           {33, 128, 128, false, 1024},
+                           {2, 32, 32, false, 512}};
+    if (force.tri_gmem) bins = {{2, INT64_MAX, 512, true, 1024}};
+    if (force.tri_small) bins = {{2, INT64_MAX, 32, false, 16}};
     for (const B& bn : bins) {
       const auto r = key_range(dkeys, bn.lo, bn.hi);
       const int64_t nf = r.second - r.first;
       if (nf <= 0) continue;
       const int cap = (int)std::min<int64_t>(bn.hi, maxD);
-      const FrameLayout L = make_layout(cap, !trisum, trisum);
+      const int hitcap = (int)(bn.hitcap * env_int("GD_TRI_HITS", 0) / 100);
+      const FrameLayout L = make_layout(cap, !trisum, trisum, hitcap);
       const int* fr = tri_frames.p + r.first;
       DBuf<char> slab;
       int grid;
@@ -1103,6 +1184,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   int64_t total_w = 0;
   for (int64_t w : wkeys) total_w += w;
   stat("wedges", total_w);
+  stat("tri_items", tot_items);
   int64_t t0 = 256, t1 = 4096, t2 = 24576;
   if (force.c4_coop || force.c4_hub32) t0 = t1 = t2 = 0;
   if (force.c4_smem) t0 = t1 = 0;  // every frame <= t2 through the u16 hash
@@ -1169,6 +1251,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       GD_CUDA(cudaMemcpyAsync(dcp.p, cpre.data(), cpre.size() * 8, cudaMemcpyHostToDevice, s));
       GD_CUDA(cudaMemcpyAsync(drch.p, rch.data(), rch.size() * 8, cudaMemcpyHostToDevice, s));
       RoundPlan P{dfr.p, dcp.p, drf.p, drch.p, (int)rf.size() - 1, F, slab_words};
+      nrounds = P.R;
       unsigned* slabs_p = slabs.p;
       unsigned* bar_p = bar.p;
       const int64_t* WP_p = WP.p;
