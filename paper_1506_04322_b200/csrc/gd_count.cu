@@ -655,16 +655,18 @@ struct RoundPlan {
   const int64_t* rch;   // [R] items per chunk of each round
   int R;                // rounds
   int F;                // max frames per round (slabs per set)
+  int T;                // independent teams of CTAs (round r belongs to team r % T)
   int64_t slab_words;   // 32-bit words per slab
 };
 
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
+// Barrier among the `members` co-resident CTAs of one team.
+__device__ __forceinline__ void team_barrier(unsigned* bar, unsigned members, unsigned& gen) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     const unsigned gen0 = gen;
     const unsigned arrived = atomicAdd(&bar[0], 1u) + 1u;
-    if (arrived == gridDim.x) {
+    if (arrived == members) {
       bar[0] = 0u;
       __threadfence();
       atomicAdd(&bar[1], 1u);
@@ -679,14 +681,13 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
 
 template <int NT, int MODE>
 __device__ void round_chunks(const View& g, const int64_t* __restrict__ WP, const RoundPlan& P,
-                             int r, unsigned* __restrict__ slabs, bool per_edge,
+                             int r, unsigned* __restrict__ set, int tb, int ts, bool per_edge,
                              u64* __restrict__ c4s, u64* __restrict__ c4tot2) {
   typedef cub::BlockReduce<u64, NT> BR;
   __shared__ typename BR::TempStorage tmp;
   const int f0 = P.rf[r], f1 = P.rf[r + 1];
   const int64_t k0 = P.cpre[f0], k1 = P.cpre[f1];
-  unsigned* set = slabs + (size_t)(r & 1) * P.F * P.slab_words;
-  for (int64_t k = k0 + blockIdx.x; k < k1; k += gridDim.x) {
+  for (int64_t k = k0 + tb; k < k1; k += ts) {
     int lo = f0, hi = f1;  // frame of chunk k: last j with cpre[j] <= k
     while (lo < hi - 1) {
       int mid = (lo + hi) >> 1;
@@ -714,23 +715,30 @@ __global__ void __launch_bounds__(NT)
 k_c4_rounds(View g, const int64_t* __restrict__ WP, RoundPlan P, unsigned* __restrict__ slabs,
             int per_edge, u64* __restrict__ c4s, u64* __restrict__ c4tot2,
             unsigned* __restrict__ bar) {
+  // teams run their rounds independently: while one team waits at its
+  // barrier, the other teams' CTAs on the same SMs keep working
+  const int team = blockIdx.x % P.T, tb = blockIdx.x / P.T;
+  const int ts = (gridDim.x - team + P.T - 1) / P.T;
+  unsigned* tbar = bar + 2 * team;
+  unsigned* sets = slabs + (size_t)team * 2 * P.F * P.slab_words;
   unsigned gen = 0;
-  for (int r = 0; r <= P.R; r++) {
-    if (r < P.R) round_chunks<NT, kCount>(g, WP, P, r, slabs, false, c4s, c4tot2);
-    if (r > 0) {
-      // zero the slabs of round r-1 with wide stores (cheaper than a zero
-      // sweep over its wedges once a round holds more wedges than counters)
-      const int used = P.rf[r] - P.rf[r - 1];
-      uint4* z = (uint4*)(slabs + (size_t)((r - 1) & 1) * P.F * P.slab_words);
+  int prev = -1, it = 0;
+  for (int r = team; ; r += P.T, it++) {
+    unsigned* set = sets + (size_t)(it & 1) * P.F * P.slab_words;
+    if (r < P.R) round_chunks<NT, kCount>(g, WP, P, r, set, tb, ts, false, c4s, c4tot2);
+    if (prev >= 0) {
+      // zero the slabs of the team's previous round with wide stores
+      const int used = P.rf[prev + 1] - P.rf[prev];
+      uint4* z = (uint4*)(sets + (size_t)((it - 1) & 1) * P.F * P.slab_words);
       const int64_t nz = (int64_t)used * P.slab_words / 4;
       const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
-      for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < nz; i += (int64_t)gridDim.x * NT)
-        z[i] = zero4;
+      for (int64_t i = tb * (int64_t)NT + threadIdx.x; i < nz; i += (int64_t)ts * NT) z[i] = zero4;
     }
-    if (r == P.R) break;
-    grid_barrier(bar, gen);
-    round_chunks<NT, kUse>(g, WP, P, r, slabs, per_edge != 0, c4s, c4tot2);
-    grid_barrier(bar, gen);
+    if (r >= P.R) break;
+    team_barrier(tbar, ts, gen);
+    round_chunks<NT, kUse>(g, WP, P, r, set, tb, ts, per_edge != 0, c4s, c4tot2);
+    team_barrier(tbar, ts, gen);
+    prev = r;
   }
 }
 
@@ -1218,9 +1226,10 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       if (per_sm < 1) throw Error(GD_ECUDA, "c4 rounds kernel cannot be resident");
       const int grid = per_sm * num_sms();
       const int64_t slab_words = (((n + 1) / 2) + 31) & ~int64_t(31);  // multiple of 4
-      const int64_t l2_budget = env_int("GD_C4_L2_MB", 128) << 20;  // per slab set
+      const int T = (int)std::max<int64_t>(1, std::min<int64_t>(grid, env_int("GD_C4_TEAMS", 4)));
+      const int64_t l2_budget = env_int("GD_C4_L2_MB", 128) << 20;  // all teams, one set each
       const int F = (int)std::max<int64_t>(
-          1, std::min<int64_t>(256, l2_budget / (slab_words * 4)));
+          1, std::min<int64_t>(256, l2_budget / (T * slab_words * 4)));
       // rounds of F frames; each round's chunk size gives >= 2 chunks per CTA
       std::vector<int> rf;
       std::vector<int64_t> rch, cpre(f16.size() + 1, 0);
@@ -1228,7 +1237,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
         const size_t j1 = std::min(f16.size(), j0 + (size_t)F);
         int64_t wr = 0;
         for (size_t j = j0; j < j1; j++) wr += w16[j];
-        int64_t ch = wr / (2 * (int64_t)grid);
+        int64_t ch = wr / (2 * (int64_t)(grid / T));
         ch = std::max<int64_t>(1024, std::min<int64_t>(65536, (ch + 511) & ~int64_t(511)));
         rf.push_back((int)j0);
         rch.push_back(ch);
@@ -1242,15 +1251,15 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       drf.alloc(rf.size(), s);
       dcp.alloc(cpre.size(), s);
       drch.alloc(rch.size(), s);
-      slabs.alloc((size_t)2 * F * slab_words, s);
+      slabs.alloc((size_t)T * 2 * F * slab_words, s);
       slabs.zero();
-      bar.alloc(2, s);
+      bar.alloc(2 * T, s);
       bar.zero();
       GD_CUDA(cudaMemcpyAsync(dfr.p, f16.data(), f16.size() * 4, cudaMemcpyHostToDevice, s));
       GD_CUDA(cudaMemcpyAsync(drf.p, rf.data(), rf.size() * 4, cudaMemcpyHostToDevice, s));
       GD_CUDA(cudaMemcpyAsync(dcp.p, cpre.data(), cpre.size() * 8, cudaMemcpyHostToDevice, s));
       GD_CUDA(cudaMemcpyAsync(drch.p, rch.data(), rch.size() * 8, cudaMemcpyHostToDevice, s));
-      RoundPlan P{dfr.p, dcp.p, drf.p, drch.p, (int)rf.size() - 1, F, slab_words};
+      RoundPlan P{dfr.p, dcp.p, drf.p, drch.p, (int)rf.size() - 1, F, T, slab_words};
       nrounds = P.R;
       unsigned* slabs_p = slabs.p;
       unsigned* bar_p = bar.p;
