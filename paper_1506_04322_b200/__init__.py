@@ -18,6 +18,11 @@ from .errors import (ClassificationError, ConsistencyError, DeviceError,
                      EdgeListParseError, GraphletError, GraphSizeError)
 from .frequencies import GraphletFrequencies
 from .graph import EdgeRef, Graph, GraphBatch, ParseOptions, order_edges_by_degree
+from .introspect import (clear_marks, clique_count, cycle_count, edge_neighborhood_census,
+                         same_side_star_edges)
+from .micro import (MICRO_CSV_HEADER, EdgeLocalCounts, MicroCounts, UnrestrictedCounts,
+                    derive_micro, micro_census, micro_counts_from_table, micro_csv,
+                    unrestricted_counts)
 from .parallel import MAX_BATCH_SIZE, ParallelConfig, WorkerFailure
 
 __version__ = "0.1.0"
@@ -34,5 +39,9 @@ __all__ = [
     "GraphletFrequencies",
     "EdgeRef", "Graph", "GraphBatch", "ParseOptions", "order_edges_by_degree",
     "MAX_BATCH_SIZE", "ParallelConfig", "WorkerFailure",
+    "MICRO_CSV_HEADER", "EdgeLocalCounts", "MicroCounts", "UnrestrictedCounts", "derive_micro",
+    "micro_census", "micro_counts_from_table", "micro_csv", "unrestricted_counts",
+    "clear_marks", "clique_count", "cycle_count", "edge_neighborhood_census",
+    "same_side_star_edges",
     "__version__",
 ]

@@ -98,6 +98,7 @@ class Graph:
         self.n = int(nn.value)
         self.m = int(mm.value)
         self._arrays: dict[str, np.ndarray] = {}
+        self._micro_cache = None
         if orig_ids is not None:
             oi = np.asarray(orig_ids, dtype=np.int64).copy()
             if len(oi) != self.n:

@@ -229,3 +229,31 @@ def make_graph_build():
 
 if __name__ == "__main__" and "--graphs" in sys.argv:
     make_graph_build()
+
+
+def make_micro_roles():
+    """Reference MicroCounts (all 14 roles) and micro_csv text for a few
+    graphs, including original-id remapping."""
+    from graphlets.census import micro_csv, micro_census, MicroCounts  # noqa: F401
+    roles = ("tt1", "tt0", "susv1", "susv0", "ts1", "ts0", "ss1", "ss0", "ti1", "ti0",
+             "si1", "si0", "ii1", "ii0")
+    out = []
+    graphs = [("paw", RG.paw_graph()), ("diamond", RG.diamond_graph()),
+              ("gnp15", RG.gnp_random_graph(15, 0.5, seed=3)),
+              ("remapped", R.Graph.from_edges(np.asarray([[100, 200], [200, 300], [300, 100],
+                                                          [300, 4000], [7, 100]])))]
+    for name, g in graphs:
+        tab = R.micro_table(g)
+        rows = []
+        for e in g.edge_refs():
+            mc = micro_census(g, e)
+            rows.append([getattr(mc, r) for r in roles] + [mc.local.indep3])
+        out.append({"name": name, "n": g.n, "edges": g.edges.tolist(),
+                    "orig_ids": g.orig_ids.tolist(), "micro": tab.tolist(), "roles": rows,
+                    "csv": micro_csv(g, tab)})
+    (HERE / "micro_roles.json").write_text(json.dumps({"roles": roles, "graphs": out}))
+    print("micro roles:", len(out))
+
+
+if __name__ == "__main__" and "--roles" in sys.argv:
+    make_micro_roles()
