@@ -55,6 +55,12 @@ SIGNATURES = (
                                         ctypes.POINTER(ctypes.c_char_p)]),
     ("gd_graph_stats", ctypes.c_int, [_vp, _i64p, ctypes.c_int,
                                       ctypes.POINTER(ctypes.c_char_p)]),
+    ("gd_comm_unique_id", ctypes.c_int, [ctypes.c_char_p]),
+    ("gd_comm_init", ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
+                                    ctypes.POINTER(_vp)]),
+    ("gd_comm_free", None, [_vp]),
+    ("gd_census_sharded", ctypes.c_int, [_vp, _vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int,
+                                         _u64p, _i64p]),
     ("gd_set_device", ctypes.c_int, [ctypes.c_int]),
     ("gd_device_alloc", _vp, [ctypes.c_int64]),
     ("gd_device_free", None, [_vp]),

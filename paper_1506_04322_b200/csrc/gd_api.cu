@@ -1,4 +1,7 @@
 // extern "C" boundary of libgdgpu.so (declared in include/gd_api.h).
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <cstring>
 #include <mutex>
 
@@ -14,9 +17,57 @@ struct gd_graph {
   std::string stats_names;
 };
 
+// NCCL is resolved at gd_comm_init (dlopen), so the library loads on hosts
+// and in processes without it; the data-path collectives are ncclAllReduce
+// (sum of per-slot uint64 counters) and ncclAllGather (128-bit totals).
+struct NcclApi {
+  ncclResult_t (*getUniqueId)(ncclUniqueId*);
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t);
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t);
+  ncclResult_t (*commDestroy)(ncclComm_t);
+  const char* (*getErrorString)(ncclResult_t);
+};
+
+struct gd_comm {
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+};
+
 namespace gd {
 
 static thread_local std::string t_last_error;
+
+static const NcclApi& nccl() {
+  static NcclApi api{};
+  static std::once_flag once;
+  static std::string err;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      err = "cannot dlopen libnccl.so.2";
+      return;
+    }
+    api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+    api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
+    api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+    api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+    api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+  });
+  if (!api.allReduce) throw Error(GD_ECUDA, err.empty() ? "NCCL symbols missing" : err);
+  return api;
+}
+
+#define GD_NCCL(call)                                                             \
+  do {                                                                            \
+    ncclResult_t _r = (call);                                                     \
+    if (_r != ncclSuccess)                                                        \
+      throw ::gd::Error(GD_ECUDA, std::string(#call) + ": " + nccl().getErrorString(_r)); \
+  } while (0)
 thread_local long long g_launches = 0;
 
 int num_sms() {
@@ -111,7 +162,7 @@ static void store_timings(gd_graph* h, CensusExtras& ex) {
 }
 
 static void census(gd_graph* h, bool per_edge, int64_t* table, int flags, uint64_t* sums,
-                   int64_t* seen) {
+                   int64_t* seen, const Shard& shard = Shard()) {
   DevGraph& g = h->g;
   cudaStream_t s = h->s;
   const int64_t G = g.G;
@@ -129,7 +180,7 @@ static void census(gd_graph* h, bool per_edge, int64_t* table, int flags, uint64
     }
   }
   CensusExtras ex;
-  run_census(g, per_edge, tptr, dsums.p, dseen.p, ex, s);
+  run_census(g, per_edge, tptr, dsums.p, dseen.p, ex, s, shard);
   std::vector<uint64_t> hs(G * 2 * kNumSums);
   std::vector<int64_t> hseen(G);
   GD_CUDA(cudaMemcpyAsync(hs.data(), dsums.p, hs.size() * 8, cudaMemcpyDeviceToHost, s));
@@ -310,6 +361,78 @@ int gd_census_per_edge_edges(const int64_t* edges, int64_t m, int64_t n, int fla
   rc = gd_census_per_edge(h, table, flags & GD_OUTPUT_DEVICE, sums, edges_seen);
   gd_graph_free(h);
   return rc;
+}
+
+int gd_comm_unique_id(unsigned char* id_out) {
+  if (!id_out) {
+    t_last_error = "id_out is NULL";
+    return GD_EINVAL;
+  }
+  return guarded([&] {
+    ncclUniqueId id;
+    GD_NCCL(nccl().getUniqueId(&id));
+    std::memcpy(id_out, id.internal, NCCL_UNIQUE_ID_BYTES);
+  });
+}
+
+int gd_comm_init(const unsigned char* id_in, int rank, int world, gd_comm** out) {
+  if (!id_in || !out || world < 1 || rank < 0 || rank >= world) {
+    t_last_error = "bad communicator arguments";
+    return GD_EINVAL;
+  }
+  *out = nullptr;
+  gd_comm* c = new gd_comm();
+  int rc = guarded([&] {
+    ncclUniqueId id;
+    std::memcpy(id.internal, id_in, NCCL_UNIQUE_ID_BYTES);
+    GD_NCCL(nccl().commInitRank(&c->comm, world, id, rank));
+    c->rank = rank;
+    c->world = world;
+  });
+  if (rc != GD_OK) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return GD_OK;
+}
+
+void gd_comm_free(gd_comm* c) {
+  if (!c) return;
+  if (c->comm) {
+    try {
+      nccl().commDestroy(c->comm);
+    } catch (...) {
+    }
+  }
+  delete c;
+}
+
+int gd_census_sharded(gd_graph* h, gd_comm* c, int virtual_ranks, int per_edge, int64_t* table,
+                      int flags, uint64_t* sums, int64_t* edges_seen) {
+  if (!h || (!c && virtual_ranks < 1)) {
+    t_last_error = "bad sharding arguments";
+    return GD_EINVAL;
+  }
+  return guarded([&] {
+    Shard sh;
+    if (c) {
+      sh.rank = c->rank;
+      sh.world = c->world;
+      cudaStream_t s = h->s;
+      ncclComm_t comm = c->comm;
+      sh.allreduce = [s, comm](unsigned long long* p, size_t count) {
+        GD_NCCL(nccl().allReduce(p, p, count, ncclUint64, ncclSum, comm, s));
+      };
+      sh.allgather = [s, comm](const unsigned long long* in, unsigned long long* out,
+                               size_t count) {
+        GD_NCCL(nccl().allGather(in, out, count, ncclUint64, comm, s));
+      };
+    } else {
+      sh.world = virtual_ranks;
+    }
+    census(h, per_edge != 0, table, flags, sums, edges_seen, sh);
+  });
 }
 
 int gd_graph_timings(const gd_graph* h, float* ms, int capacity, const char** names) {

@@ -317,12 +317,12 @@ __device__ void tri_frame(const View& g, int a, char* mem, const FrameLayout& L,
 
 template <int NT>
 __global__ void __launch_bounds__(NT)
-k_tri_frames(View g, const int* __restrict__ frames, int nframes, FrameLayout L, char* gslab,
-             const int64_t* __restrict__ OP, u64* __restrict__ tcs, u64* __restrict__ vT,
-             u64* __restrict__ k4tot) {
+k_tri_frames(View g, const int* __restrict__ frames, int nframes, int rank, int world,
+             FrameLayout L, char* gslab, const int64_t* __restrict__ OP, u64* __restrict__ tcs,
+             u64* __restrict__ vT, u64* __restrict__ k4tot) {
   extern __shared__ __align__(16) char smem[];
   char* mem = gslab ? gslab + (size_t)blockIdx.x * L.bytes : smem;
-  for (int f = blockIdx.x; f < nframes; f += gridDim.x)
+  for (int f = rank + world * blockIdx.x; f < nframes; f += world * gridDim.x)
     tri_frame<NT>(g, frames[f], mem, L, OP, tcs, vT, k4tot);
 }
 
@@ -382,12 +382,13 @@ __device__ void trisum_frame(const View& g, int a, char* mem, const FrameLayout&
 
 template <int NT>
 __global__ void __launch_bounds__(NT)
-k_trisum_frames(View g, const int* __restrict__ frames, int nframes, FrameLayout L, char* gslab,
-                const int64_t* __restrict__ OP, const u64* __restrict__ tcs,
-                u64* __restrict__ tsl, u64* __restrict__ tsh, u64* __restrict__ tsd) {
+k_trisum_frames(View g, const int* __restrict__ frames, int nframes, int rank, int world,
+                FrameLayout L, char* gslab, const int64_t* __restrict__ OP,
+                const u64* __restrict__ tcs, u64* __restrict__ tsl, u64* __restrict__ tsh,
+                u64* __restrict__ tsd) {
   extern __shared__ __align__(16) char smem[];
   char* mem = gslab ? gslab + (size_t)blockIdx.x * L.bytes : smem;
-  for (int f = blockIdx.x; f < nframes; f += gridDim.x)
+  for (int f = rank + world * blockIdx.x; f < nframes; f += world * gridDim.x)
     trisum_frame<NT>(g, frames[f], mem, L, OP, tcs, tsl, tsh, tsd);
 }
 
@@ -576,14 +577,14 @@ __device__ u64 wedge_sweep(const View& g, const int64_t* __restrict__ WP, int64_
 template <int NT, bool C16>
 __global__ void __launch_bounds__(NT)
 k_c4_frames_smem(View g, const int64_t* __restrict__ WP, const int* __restrict__ frames,
-                 int nframes, int hcap, int per_edge, u64* __restrict__ c4s,
+                 int nframes, int rank, int world, int hcap, int per_edge, u64* __restrict__ c4s,
                  u64* __restrict__ c4tot2) {
   extern __shared__ __align__(16) char smem[];
   int* hk = (int*)smem;
   unsigned* hv = (unsigned*)(hk + hcap);
   typedef cub::BlockReduce<u64, NT> BR;
   __shared__ typename BR::TempStorage tmp;
-  for (int f = blockIdx.x; f < nframes; f += gridDim.x) {
+  for (int f = rank + world * blockIdx.x; f < nframes; f += world * gridDim.x) {
     const int s = frames[f];
     const int64_t b = g.rp[s], o = g.osplit[s];
     const int64_t i0 = WP[b], i1 = WP[o];
@@ -1052,8 +1053,13 @@ std::pair<int64_t, int64_t> key_range(const std::vector<int64_t>& keys, int64_t 
 // Host orchestration
 // ---------------------------------------------------------------------------
 void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long long* sums_dev,
-                unsigned long long* seen_dev, CensusExtras& ex, cudaStream_t s) {
+                unsigned long long* seen_dev, CensusExtras& ex, cudaStream_t s, const Shard& sh) {
   const ForcePaths force = read_force();
+  // shards executed by this process: its own (multi-GPU) or all (emulated)
+  const int world = std::max(1, sh.world);
+  std::vector<int> my_ranks;
+  if (sh.real()) my_ranks.push_back(sh.rank);
+  else for (int r = 0; r < world; r++) my_ranks.push_back(r);
   const long long launches0 = g_launches;
   const int64_t n = g.n, m = g.m, G = g.G, S = 2 * m;
   const View v = make_view(g);
@@ -1142,26 +1148,28 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       const int hitcap = (int)(bn.hitcap * env_int("GD_TRI_HITS", 0) / 100);
       const FrameLayout L = make_layout(cap, !trisum, trisum, hitcap);
       const int* fr = tri_frames.p + r.first;
+      const int64_t per_rank = (nf + world - 1) / world;
       DBuf<char> slab;
       int grid;
       if (bn.gmem) {
-        grid = (int)std::min<int64_t>(nf, 2 * num_sms());
+        grid = (int)std::min<int64_t>(per_rank, 2 * num_sms());
         slab.alloc((size_t)grid * L.bytes, s);
       } else {
-        grid = (int)std::min<int64_t>(nf, (int64_t)num_sms() * 64);
+        grid = (int)std::min<int64_t>(per_rank, (int64_t)num_sms() * 64);
       }
       char* sp = bn.gmem ? slab.p : nullptr;
       const size_t sm = sp ? 0 : L.bytes;
+      for (const int rk : my_ranks) {
 #define GD_TRI_LAUNCH(NTV)                                                                   \
   if (!trisum) {                                                                             \
     set_smem(k_tri_frames<NTV>, sm);                                                         \
-    k_tri_frames<NTV><<<grid, NTV, sm, s>>>(v, fr, (int)nf, L, sp, OP.p, tcs.p, vT.p,         \
-                                            k4tot.p);                                        \
+    k_tri_frames<NTV><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp, OP.p, tcs.p,    \
+                                            vT.p, k4tot.p);                                  \
     GD_LAUNCH_CHECK("tri_frames");                                                           \
   } else {                                                                                   \
     set_smem(k_trisum_frames<NTV>, sm);                                                      \
-    k_trisum_frames<NTV><<<grid, NTV, sm, s>>>(v, fr, (int)nf, L, sp, OP.p, tcs.p, tsl.p,     \
-                                               tsh.p, tsd.p);                                \
+    k_trisum_frames<NTV><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp, OP.p, tcs.p, \
+                                               tsl.p, tsh.p, tsd.p);                         \
     GD_LAUNCH_CHECK("trisum_frames");                                                        \
   }
       switch (bn.nt) {
@@ -1170,11 +1178,17 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
         case 128: GD_TRI_LAUNCH(128) break;
         default: GD_TRI_LAUNCH(32) break;
       }
+      }
 #undef GD_TRI_LAUNCH
     }
   };
   run_frames(false);
   timer.mark("tri_frames");
+  if (sh.real()) {  // per-slot triangle / 4-clique counts and T(x) of all shards
+    sh.allreduce(tcs.p, (size_t)S);
+    sh.allreduce(vT.p, (size_t)n);
+    timer.mark("allreduce_a");
+  }
   if (n) {
     k_vertex_s<<<grid_cap(n * 32, 256), 256, 0, s>>>(v, vS.p);
     GD_LAUNCH_CHECK("vertex_s");
@@ -1208,17 +1222,30 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     std::vector<int> hf(nh);
     GD_CUDA(cudaMemcpyAsync(hf.data(), c4_frames.p + rh.first, nh * 4, cudaMemcpyDeviceToHost, s));
     GD_CUDA(cudaStreamSynchronize(s));
-    std::vector<int> f16, f32;
-    std::vector<int64_t> w16;
+    std::vector<int> f16_all, f32_all;
+    std::vector<int64_t> w16_all, h16, h32;
     for (int64_t h = 0; h < nh; h++) {
       if (wbig[rh.first + h] || force.c4_hub32) {
-        f32.push_back(hf[h]);
+        f32_all.push_back(hf[h]);
+        h32.push_back(h);
       } else {
-        f16.push_back(hf[h]);
-        w16.push_back(wkeys[rh.first + h]);
+        f16_all.push_back(hf[h]);
+        w16_all.push_back(wkeys[rh.first + h]);
+        h16.push_back(h);
       }
     }
-    n32 = (int64_t)f32.size();
+    n32 = (int64_t)f32_all.size();
+    for (const int rk : my_ranks) {
+    // this shard's frames: every world-th heavy frame in descending-work order
+    std::vector<int> f16, f32;
+    std::vector<int64_t> w16;
+    for (size_t i = 0; i < f16_all.size(); i++)
+      if ((int)(h16[i] % world) == rk) {
+        f16.push_back(f16_all[i]);
+        w16.push_back(w16_all[i]);
+      }
+    for (size_t i = 0; i < f32_all.size(); i++)
+      if ((int)(h32[i] % world) == rk) f32.push_back(f32_all[i]);
     if (!f16.empty()) {
       constexpr int NT = 512;
       int per_sm = 0;
@@ -1260,7 +1287,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       GD_CUDA(cudaMemcpyAsync(dcp.p, cpre.data(), cpre.size() * 8, cudaMemcpyHostToDevice, s));
       GD_CUDA(cudaMemcpyAsync(drch.p, rch.data(), rch.size() * 8, cudaMemcpyHostToDevice, s));
       RoundPlan P{dfr.p, dcp.p, drf.p, drch.p, (int)rf.size() - 1, F, T, slab_words};
-      nrounds = P.R;
+      nrounds += P.R;
       unsigned* slabs_p = slabs.p;
       unsigned* bar_p = bar.p;
       const int64_t* WP_p = WP.p;
@@ -1311,6 +1338,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       }
       timer.mark("c4_hub32");
     }
+    }  // shards
   }
   auto smem_bin = [&](std::pair<int64_t, int64_t> r, auto kernel, int nt, bool c16, int per_sm) {
     const int64_t nf = r.second - r.first;
@@ -1322,15 +1350,25 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     const size_t sm = (size_t)hcap * 4 + (size_t)hcap * (c16 ? 2 : 4);
     if (sm > 200 * 1024) throw Error(GD_EINVAL, "wedge frame too large for the shared hash");
     set_smem(kernel, sm);
-    const int grid = (int)std::min<int64_t>(nf, (int64_t)num_sms() * per_sm);
-    kernel<<<grid, nt, sm, s>>>(v, WP.p, c4_frames.p + r.first, (int)nf, hcap, pe, c4s_p,
-                                c4tot2.p);
-    GD_LAUNCH_CHECK("c4_frames_smem");
+    const int grid =
+        (int)std::min<int64_t>((nf + world - 1) / world, (int64_t)num_sms() * per_sm);
+    for (const int rk : my_ranks) {
+      kernel<<<grid, nt, sm, s>>>(v, WP.p, c4_frames.p + r.first, (int)nf, rk, world, hcap, pe,
+                                  c4s_p, c4tot2.p);
+      GD_LAUNCH_CHECK("c4_frames_smem");
+    }
   };
   smem_bin(rs2, k_c4_frames_smem<512, true>, 512, true, 1);
   smem_bin(rs1, k_c4_frames_smem<256, false>, 256, false, 3);
   smem_bin(rs0, k_c4_frames_smem<64, false>, 64, false, 32);
   timer.mark("c4_smem");
+  if (sh.real() && per_edge) {  // per-slot triangle sums and 4-cycle counts of all shards
+    sh.allreduce(tsl.p, (size_t)S);
+    sh.allreduce(tsh.p, (size_t)S);
+    sh.allreduce(tsd.p, (size_t)S);
+    sh.allreduce(c4s.p, (size_t)S);
+    timer.mark("allreduce_bc");
+  }
   stat("c4_coop_frames", nh - n32);
   stat("c4_rounds", nrounds);
   stat("c4_u32_hub_frames", n32);
@@ -1367,14 +1405,32 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   }
   timer.mark("finalize");
 
-  std::vector<u64> hk4(2 * G), hc4(2 * G);
-  GD_CUDA(cudaMemcpyAsync(hk4.data(), k4tot.p, 2 * G * 8, cudaMemcpyDeviceToHost, s));
-  GD_CUDA(cudaMemcpyAsync(hc4.data(), c4tot2.p, 2 * G * 8, cudaMemcpyDeviceToHost, s));
+  // per-shard 128-bit totals: gathered (not summed) so carries stay exact
+  const int nranks = sh.real() ? world : 1;
+  std::vector<u64> hk4(2 * G * nranks), hc4(2 * G * nranks);
+  if (sh.real()) {
+    DBuf<u64> gk4, gc4;
+    gk4.alloc(2 * G * nranks, s);
+    gc4.alloc(2 * G * nranks, s);
+    sh.allgather(k4tot.p, gk4.p, (size_t)(2 * G));
+    sh.allgather(c4tot2.p, gc4.p, (size_t)(2 * G));
+    GD_CUDA(cudaMemcpyAsync(hk4.data(), gk4.p, hk4.size() * 8, cudaMemcpyDeviceToHost, s));
+    GD_CUDA(cudaMemcpyAsync(hc4.data(), gc4.p, hc4.size() * 8, cudaMemcpyDeviceToHost, s));
+    GD_CUDA(cudaStreamSynchronize(s));
+  } else {
+    GD_CUDA(cudaMemcpyAsync(hk4.data(), k4tot.p, 2 * G * 8, cudaMemcpyDeviceToHost, s));
+    GD_CUDA(cudaMemcpyAsync(hc4.data(), c4tot2.p, 2 * G * 8, cudaMemcpyDeviceToHost, s));
+  }
   timer.collect(ex.ms, ex.names);
   stat("launches", g_launches - launches0);
-  for (int64_t i = 0; i < G; i++) {
-    ex.k4tot[i] = ((u128)hk4[2 * i + 1] << 64) | hk4[2 * i];
-    ex.c4tot2[i] = ((u128)hc4[2 * i + 1] << 64) | hc4[2 * i];
+  stat("shards", world);
+  for (int r = 0; r < nranks; r++) {
+    const u64* a = hk4.data() + 2 * G * r;
+    const u64* c = hc4.data() + 2 * G * r;
+    for (int64_t i = 0; i < G; i++) {
+      ex.k4tot[i] += ((u128)a[2 * i + 1] << 64) | a[2 * i];
+      ex.c4tot2[i] += ((u128)c[2 * i + 1] << 64) | c[2 * i];
+    }
   }
 }
 

@@ -197,3 +197,28 @@ def test_config3_rmat20_full_size():
 def test_config5_chung_lu_4m_full_size():
     g, f = _big_parity("c5_chung_lu_4m", 100)
     assert g.n == 4_000_000
+
+
+@pytest.mark.parametrize("force", ["", "tri_gmem,c4_coop", "c4_hub32"])
+def test_emulated_shards_match(force):
+    """Frame sharding (multi-GPU partition) emulated on one GPU: every shard
+    count gives the unsharded result bit for bit."""
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import paper_1506_04322_b200 as gd
+from paper_1506_04322_b200.distributed import graphlet_census_sharded, micro_census_table_sharded
+import test_gpu_parity as T
+for name, n, edges in T._dense_cases():
+    g = gd.Graph(n, edges)
+    tab, f = gd.micro_census_table(g)
+    for k in (2, 3, 5):
+        assert graphlet_census_sharded(g, None, k) == f, (name, k)
+        t2, f2 = micro_census_table_sharded(g, None, k)
+        assert f2 == f and np.array_equal(np.asarray(t2), np.asarray(tab)), (name, k)
+print("ok")
+''' % (str(GOLDEN.parent.parent), str(GOLDEN.parent))
+    env = dict(os.environ, GD_FORCE_PATH=force)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
