@@ -146,16 +146,18 @@ def measured_peak():
 
 
 def ncu_traffic(config: str, mode: str):
-    """Per-census DRAM bytes of the dominant kernel from the committed ncu
-    capture summary (profiles/ncu_summary.json), if one exists."""
+    """DRAM bytes (read + write) of one census, summed over its kernels, and
+    the top kernel with its time share, from the committed ncu launch list
+    summary (profiles/ncu_summary.json, made by tools/ncu_sum.py)."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
         return None, None
     try:
-        d = json.loads(p.read_text())
-        e = d[f"{config}/{mode}"]
-        return e.get("dram_bytes_per_launch"), e.get("kernel")
-    except (KeyError, ValueError):
+        e = json.loads(p.read_text())[f"{config}/{mode}"]
+        top = next(iter(e["kernels"].items()))
+        return e["census_dram_bytes"], {"name": top[0], "share": top[1]["share"],
+                                        "dram_bytes": top[1]["dram_bytes"]}
+    except (KeyError, ValueError, StopIteration):
         return None, None
 
 
