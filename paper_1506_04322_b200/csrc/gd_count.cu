@@ -30,9 +30,12 @@
 #include <algorithm>
 #include <functional>
 
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "gd_count.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace gd {
 
@@ -643,6 +646,72 @@ k_c4_hub(View g, const int64_t* __restrict__ WP, const HubChunk* __restrict__ ch
   }
 }
 
+// Heavy frames on thread-block clusters: the dense u16 counter array of one
+// frame (one counter per rank id < n) is spread over the distributed shared
+// memory of a cluster of `csize` CTAs (counter x lives in CTA x / per).  The
+// count sweep is remote shared-memory atomics, the use sweep remote reads;
+// no counter ever touches L2/HBM, which stays free for the adjacency rows.
+// Each cluster takes frames (descending work) from a global queue.
+struct DsmemCounter {
+  unsigned* base;  // this CTA's slab (same offset in every CTA of the cluster)
+  int per;         // counters per CTA (even)
+  __device__ __forceinline__ void inc(int x) const {
+    const int owner = x / per, off = x - owner * per;
+    unsigned* w = cg::this_cluster().map_shared_rank(base, owner) + (off >> 1);
+    atomicAdd(w, 1u << ((off & 1) << 4));
+  }
+  __device__ __forceinline__ unsigned get(int x) const {
+    const int owner = x / per, off = x - owner * per;
+    const unsigned short* c =
+        (const unsigned short*)cg::this_cluster().map_shared_rank(base, owner);
+    return c[off];
+  }
+  __device__ __forceinline__ unsigned take(int x) const { return get(x); }  // unused
+  __device__ __forceinline__ void zero(int) const {}
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 1)
+k_c4_cluster(View g, const int64_t* __restrict__ WP, const int* __restrict__ frames,
+             int nframes, int rank, int world, int* __restrict__ queue, int per, int per_edge,
+             u64* __restrict__ c4s, u64* __restrict__ c4tot2) {
+  extern __shared__ __align__(16) unsigned slab[];
+  __shared__ int s_frame;
+  typedef cub::BlockReduce<u64, NT> BR;
+  __shared__ typename BR::TempStorage tmp;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank(), csize = (int)cluster.num_blocks();
+  const int words = per >> 1;
+  uint4* z4 = (uint4*)slab;
+  for (int i = threadIdx.x; i < words / 4; i += NT) z4[i] = make_uint4(0u, 0u, 0u, 0u);
+  DsmemCounter ctr{slab, per};
+  while (true) {
+    if (crank == 0 && threadIdx.x == 0) {
+      const int q = atomicAdd(queue, 1);
+      s_frame = rank + world * q;  // this shard's frames: every world-th
+    }
+    cluster.sync();  // counters zeroed everywhere, frame published
+    const int f = *cluster.map_shared_rank(&s_frame, 0);
+    // no CTA may exit (or rank 0 republish) while another still reads s_frame
+    cluster.sync();
+    if (f >= nframes) break;
+    const int s = frames[f];
+    const int64_t b = g.rp[s], o = g.osplit[s];
+    const int64_t fi0 = WP[b], fi1 = WP[o];
+    const int64_t len = (fi1 - fi0 + csize - 1) / csize;
+    const int64_t i0 = fi0 + len * crank;
+    const int64_t i1 = i0 + len < fi1 ? i0 + len : fi1;
+    if (i0 < i1) wedge_sweep<NT, kCount>(g, WP, b, o, i0, i1, ctr, false, c4s);
+    cluster.sync();
+    const u64 local =
+        i0 < i1 ? wedge_sweep<NT, kUse>(g, WP, b, o, i0, i1, ctr, per_edge != 0, c4s) : 0;
+    const u64 sum = BR(tmp).Sum(local);
+    if (threadIdx.x == 0 && sum) atomic_add_u128(c4tot2 + 2 * graph_of(g, s), sum);
+    cluster.sync();  // every remote read of this frame done
+    for (int i = threadIdx.x; i < words / 4; i += NT) z4[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+
 // Cooperative rounds for the heavy frames.  All CTAs are co-resident
 // (cooperative launch) and walk the same round schedule: a round is up to F
 // frames whose u16 counter slabs stay L2-resident; its items are cut into
@@ -1246,7 +1315,59 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       }
     for (size_t i = 0; i < f32_all.size(); i++)
       if ((int)(h32[i] % world) == rk) f32.push_back(f32_all[i]);
-    if (!f16.empty()) {
+    // dense counters in cluster shared memory when n fits in <= 4 CTAs (wider
+    // clusters measured slower than the L2 rounds: hot counters serialise
+    // on one SM's shared memory and only 7 16-CTA clusters are resident)
+    int csize = 0, per = 0;
+    if (env_int("GD_C4_CLUSTER", 1)) {
+      const int64_t max_per = 98304;  // u16 counters per CTA (192 KB)
+      const int cmax = (int)env_int("GD_C4_CLUSTER_MAX", 4);
+      for (int c = 1; c <= cmax; c *= 2) {
+        const int64_t p = (((n + c - 1) / c) + 7) & ~int64_t(7);
+        if (p <= max_per) {
+          csize = c;
+          per = (int)p;
+          break;
+        }
+      }
+    }
+    if (!f16.empty() && csize) {
+      constexpr int NT = 512;
+      const size_t sm = (size_t)per * 2;
+      auto kern = k_c4_cluster<NT>;
+      set_smem(kern, sm);
+      if (csize > 8)
+        GD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = csize;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.blockDim = dim3(NT);
+      cfg.dynamicSmemBytes = sm;
+      cfg.stream = s;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cfg.gridDim = dim3(csize);
+      int nclusters = 0;
+      GD_CUDA(cudaOccupancyMaxActiveClusters(&nclusters, (void*)kern, &cfg));
+      if (nclusters < 1) throw Error(GD_ECUDA, "cluster kernel cannot be resident");
+      cfg.gridDim = dim3(nclusters * csize);
+      DBuf<int> dfr, queue;
+      dfr.alloc(f16_all.size(), s);
+      queue.alloc(1, s);
+      queue.zero();
+      GD_CUDA(cudaMemcpyAsync(dfr.p, f16_all.data(), f16_all.size() * 4, cudaMemcpyHostToDevice,
+                              s));
+      const int* WPc = nullptr;
+      (void)WPc;
+      GD_CUDA(cudaLaunchKernelEx(&cfg, kern, v, (const int64_t*)WP.p, (const int*)dfr.p,
+                                 (int)f16_all.size(), rk, world, queue.p, per, pe, c4s_p,
+                                 c4tot2.p));
+      GD_LAUNCH_CHECK("c4_cluster");
+      nrounds = -csize;  // reported as the cluster size
+    } else if (!f16.empty()) {
       constexpr int NT = 512;
       int per_sm = 0;
       GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_c4_rounds<NT>, NT, 0));
