@@ -73,22 +73,20 @@ typedef unsigned __int128 u128;
 struct FrameLayout {
   int cap;     // max frame size D
   int hcap;    // hash capacity (pow2 >= 2*cap)
-  int hitcap;  // local-edge (hit) list capacity, 0 = none
   int rows;    // 1: pass-A bitmap rows
   int accum;   // 1: pass-B accumulators
-  size_t o_qb, o_lv, o_p, o_hk, o_hv, o_rows, o_tri2, o_hits, o_tl, o_dl, o_acc;
+  size_t o_qb, o_lv, o_p, o_hk, o_hv, o_rows, o_tri2, o_tl, o_dl, o_acc;
   size_t bytes;
 };
 
 __host__ __device__ __forceinline__ int row_stride64(int W) { return W | 1; }
 
-FrameLayout make_layout(int cap, bool rows, bool accum, int hitcap) {
+FrameLayout make_layout(int cap, bool rows, bool accum) {
   FrameLayout L{};
   L.cap = cap;
   int h = 32;
   while (h < 2 * cap) h <<= 1;
   L.hcap = h;
-  L.hitcap = rows ? hitcap : 0;
   L.rows = rows;
   L.accum = accum;
   size_t o = 0;
@@ -103,7 +101,6 @@ FrameLayout make_layout(int cap, bool rows, bool accum, int hitcap) {
     const int W = (cap + 63) / 64;
     L.o_rows = take(8ull * cap * row_stride64(W));
   }
-  if (L.hitcap) L.o_hits = take(8ull * L.hitcap);
   L.o_lv = take(4 * (size_t)cap);
   L.o_p = take(4 * (size_t)(cap + 1));
   L.o_hk = take(4 * (size_t)h);
@@ -225,14 +222,31 @@ __device__ __forceinline__ u64 pack_hit(int j, int k, int i) {
   return ((u64)(unsigned)j << 48) | ((u64)(unsigned)k << 32) | (u64)(unsigned)i;
 }
 
+// Local-edge (hit) lists.  Sweep 1 of a triangle frame appends every local
+// edge (j, k, item i) to a per-CTA staging list in global memory (L2-hot);
+// sweep 2 then walks the list instead of probing every item again.  In
+// per-edge mode the list is copied to an exact-size slice of a graph-wide
+// hit buffer (bump allocated) so pass B needs no probing at all.  A frame
+// whose list overflows staging or the hit buffer falls back to probing.
+struct HitLists {
+  u64* stage;          // [grid][stage_cap] staging lists
+  int stage_cap;       // entries per CTA (0: no lists)
+  u64* buf;            // graph-wide hit buffer (null: do not persist)
+  u64* top;            // bump pointer into buf
+  u64 cap;             // entries in buf
+  int64_t* hoff;       // [n] frame -> first entry in buf
+  int* hcnt;           // [n] frame -> entries, -1 = not persisted
+};
+
 // ------------------------------------------------------------------------
 // pass A
 // ------------------------------------------------------------------------
 template <int NT>
 __device__ void tri_frame(const View& g, int a, char* mem, const FrameLayout& L,
                           const int64_t* __restrict__ OP, u64* __restrict__ tcs,
-                          u64* __restrict__ vT, u64* __restrict__ k4tot) {
+                          u64* __restrict__ vT, u64* __restrict__ k4tot, const HitLists& HL) {
   __shared__ int nhits;
+  __shared__ u64 s_off;
   LocalHash H;
   const int D = frame_load<NT>(g, a, mem, L, OP, H);
   const int* Lv = (const int*)(mem + L.o_lv);
@@ -240,7 +254,7 @@ __device__ void tri_frame(const View& g, int a, char* mem, const FrameLayout& L,
   const int64_t* QB = (const int64_t*)(mem + L.o_qb);
   u64* rows = (u64*)(mem + L.o_rows);
   unsigned* tri2 = (unsigned*)(mem + L.o_tri2);
-  u64* hits = (u64*)(mem + L.o_hits);
+  u64* hits = HL.stage ? HL.stage + (size_t)blockIdx.x * HL.stage_cap : nullptr;
   const int W = (D + 63) >> 6;
   const int RS = row_stride64(W);
   for (int i = threadIdx.x; i < D * RS; i += NT) rows[i] = 0ull;
@@ -248,7 +262,7 @@ __device__ void tri_frame(const View& g, int a, char* mem, const FrameLayout& L,
   if (threadIdx.x == 0) nhits = 0;
   __syncthreads();
   const int total = P[D];
-  const int hitcap = (D < 65536) ? L.hitcap : 0;
+  const int hitcap = (hits && D < 65536) ? HL.stage_cap : 0;
   // sweep 1: local adjacency bitmaps (undirected) + the list of local edges
   for_frame_items<NT>(g, P, QB, D, total, [&](int j, int i, int64_t, int y) {
     const int k = H.find(y);
@@ -266,6 +280,19 @@ __device__ void tri_frame(const View& g, int a, char* mem, const FrameLayout& L,
     }
   });
   __syncthreads();
+  const int nh = nhits;
+  const bool listed = hitcap > 0 && nh <= hitcap;
+  // persist the list for pass B (exact-size bump allocation)
+  if (HL.buf && threadIdx.x == 0) {
+    u64 off = ~0ull;
+    if (listed && nh > 0) {
+      off = atomicAdd(HL.top, (u64)nh);
+      if (off + (u64)nh > HL.cap) off = ~0ull;
+    }
+    s_off = off;
+    HL.hoff[a] = (int64_t)off;
+    HL.hcnt[a] = (listed && (nh == 0 || off != ~0ull)) ? nh : -1;
+  }
   // sweep 2: each local edge (x_j, x_k) is the triangle {a, x_j, x_k}; its
   // common local neighbours are the 4-cliques {a, x_j, x_k, z}
   auto local_edge = [&](int j, int k, int64_t q) {
@@ -279,10 +306,13 @@ __device__ void tri_frame(const View& g, int a, char* mem, const FrameLayout& L,
       atomicAdd(&tri2[k], c);
     }
   };
-  const int nh = nhits;
-  if (hitcap > 0 && nh <= hitcap) {
+  if (listed) {
+    __syncthreads();
+    const u64 off = HL.buf ? s_off : ~0ull;
+    u64* dst = off != ~0ull ? HL.buf + off : nullptr;
     for (int h = threadIdx.x; h < nh; h += NT) {
       const u64 e = hits[h];
+      if (dst) dst[h] = e;
       const int j = (int)(e >> 48), k = (int)((e >> 32) & 0xffff), i = (int)(unsigned)e;
       local_edge(j, k, QB[j] + i);
     }
@@ -322,22 +352,23 @@ template <int NT>
 __global__ void __launch_bounds__(NT)
 k_tri_frames(View g, const int* __restrict__ frames, int nframes, int rank, int world,
              FrameLayout L, char* gslab, const int64_t* __restrict__ OP, u64* __restrict__ tcs,
-             u64* __restrict__ vT, u64* __restrict__ k4tot) {
+             u64* __restrict__ vT, u64* __restrict__ k4tot, HitLists HL) {
   extern __shared__ __align__(16) char smem[];
   char* mem = gslab ? gslab + (size_t)blockIdx.x * L.bytes : smem;
   for (int f = rank + world * blockIdx.x; f < nframes; f += world * gridDim.x)
-    tri_frame<NT>(g, frames[f], mem, L, OP, tcs, vT, k4tot);
+    tri_frame<NT>(g, frames[f], mem, L, OP, tcs, vT, k4tot, HL);
 }
 
 // ------------------------------------------------------------------------
 // pass B: per out-slot sums over the triangle set, by rank side
 //   tsl: sum t(lo, w)   tsh: sum t(hi, w)   tsd: sum d(w)   (w in Tri_e)
+// Frames with a persisted hit list walk it; the others probe again.
 // ------------------------------------------------------------------------
 template <int NT>
 __device__ void trisum_frame(const View& g, int a, char* mem, const FrameLayout& L,
                              const int64_t* __restrict__ OP, const u64* __restrict__ tcs,
                              u64* __restrict__ tsl, u64* __restrict__ tsh,
-                             u64* __restrict__ tsd) {
+                             u64* __restrict__ tsd, const HitLists& HL) {
   LocalHash H;
   const int D = frame_load<NT>(g, a, mem, L, OP, H);
   const int* Lv = (const int*)(mem + L.o_lv);
@@ -357,9 +388,7 @@ __device__ void trisum_frame(const View& g, int a, char* mem, const FrameLayout&
   __syncthreads();
   const int total = P[D];
   const u64 deg_a = (u64)g.deg[a];
-  for_frame_items<NT>(g, P, QB, D, total, [&](int j, int, int64_t q, int y) {
-    const int k = H.find(y);
-    if (k < 0) return;
+  auto local_edge = [&](int j, int k, int64_t q) {
     const u64 t_jk = tcs[q] >> kTriShift;
     // edge (x_j, x_k), lo side x_j, third vertex a
     atomicAdd(&tsl[q], (u64)tL[j]);
@@ -372,7 +401,21 @@ __device__ void trisum_frame(const View& g, int a, char* mem, const FrameLayout&
     atomicAdd(&acc[3 * k], (u64)tL[j]);
     atomicAdd(&acc[3 * k + 1], t_jk);
     atomicAdd(&acc[3 * k + 2], (u64)dL[j]);
-  });
+  };
+  const int nh = HL.hcnt ? HL.hcnt[a] : -1;
+  if (nh >= 0) {
+    const u64* src = HL.buf + HL.hoff[a];
+    for (int h = threadIdx.x; h < nh; h += NT) {
+      const u64 e = src[h];
+      const int j = (int)(e >> 48), k = (int)((e >> 32) & 0xffff), i = (int)(unsigned)e;
+      local_edge(j, k, QB[j] + i);
+    }
+  } else {
+    for_frame_items<NT>(g, P, QB, D, total, [&](int j, int, int64_t q, int y) {
+      const int k = H.find(y);
+      if (k >= 0) local_edge(j, k, q);
+    });
+  }
   __syncthreads();
   for (int j = threadIdx.x; j < D; j += NT) {
     if (acc[3 * j + 2] == 0) continue;  // no triangle on edge (a, x_j)
@@ -388,11 +431,25 @@ __global__ void __launch_bounds__(NT)
 k_trisum_frames(View g, const int* __restrict__ frames, int nframes, int rank, int world,
                 FrameLayout L, char* gslab, const int64_t* __restrict__ OP,
                 const u64* __restrict__ tcs, u64* __restrict__ tsl, u64* __restrict__ tsh,
-                u64* __restrict__ tsd) {
+                u64* __restrict__ tsd, HitLists HL) {
   extern __shared__ __align__(16) char smem[];
   char* mem = gslab ? gslab + (size_t)blockIdx.x * L.bytes : smem;
   for (int f = rank + world * blockIdx.x; f < nframes; f += world * gridDim.x)
-    trisum_frame<NT>(g, frames[f], mem, L, OP, tcs, tsl, tsh, tsd);
+    trisum_frame<NT>(g, frames[f], mem, L, OP, tcs, tsl, tsh, tsd, HL);
+}
+
+// Upper bound of the local-edge count of all frames: sum_a min(items_a, C(D_a, 2)).
+__global__ void k_hit_bound(View g, const int64_t* __restrict__ OP, u64* __restrict__ out) {
+  u64 acc = 0;
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < g.n;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = g.osplit[a], e = g.rp[a + 1];
+    const u64 D = (u64)(e - b), items = (u64)(OP[e] - OP[b]);
+    const u64 c2 = D * (D - (D > 0)) / 2;
+    acc += items < c2 ? items : c2;
+  }
+  for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
 }
 
 // ------------------------------------------------------------------------
@@ -1200,45 +1257,101 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
 
   // ---- pass A / pass B: triangle frames by D = |N+(a)| ----------------------
   const int64_t maxD = dkeys.empty() ? 0 : dkeys[0];
+  // graph-wide hit buffer (per-edge mode): exact-size lists for pass B,
+  // capacity = min(sum_a min(items_a, C(D_a, 2)), 35% of free memory)
+  const bool lists = env_int("GD_TRI_LISTS", 1) != 0;
+  DBuf<u64> hitbuf, hittop;
+  DBuf<int64_t> hoff;
+  DBuf<int> hcnt;
+  u64 hit_cap = 0;
+  if (per_edge && lists && n) {
+    DBuf<u64> bound;
+    bound.alloc(1, s);
+    bound.zero();
+    k_hit_bound<<<grid_cap(n, 256), 256, 0, s>>>(v, OP.p, bound.p);
+    GD_LAUNCH_CHECK("hit_bound");
+    u64 hb = 0;
+    GD_CUDA(cudaMemcpyAsync(&hb, bound.p, 8, cudaMemcpyDeviceToHost, s));
+    GD_CUDA(cudaStreamSynchronize(s));
+    size_t fr = 0, tot = 0;
+    GD_CUDA(cudaMemGetInfo(&fr, &tot));
+    hit_cap = std::min<u64>(hb, (u64)(fr * 0.35) / 8);
+    hit_cap = std::min<u64>(hit_cap, (u64)env_int("GD_HIT_CAP", INT64_MAX));  // tests
+    if (hit_cap) {
+      hitbuf.alloc(hit_cap, s);
+      hittop.alloc(1, s);
+      hittop.zero();
+      hoff.alloc(n, s);
+      hcnt.alloc(n, s);
+      GD_CUDA(cudaMemsetAsync(hcnt.p, 0xff, n * sizeof(int), s));  // -1: not persisted
+    }
+    stat("hit_buffer_entries", (int64_t)hit_cap);
+  }
   auto run_frames = [&](bool trisum) {
-    struct B { int64_t lo, hi; int nt; bool gmem; int hitcap; };
-    std::vector<B> bins = {{1025, INT64_MAX, 512, true, 65536},
-                           {513, 1024, 512, false, 4096},
-                           {129, 512, 256, false, 4096},
-                           {33, 128, 128, false, 1024},
-                           {2, 32, 32, false, 512}};
-    if (force.tri_gmem) bins = {{2, INT64_MAX, 512, true, 1024}};
-    if (force.tri_small) bins = {{2, INT64_MAX, 32, false, 16}};
+    struct B { int64_t lo, hi; int nt; bool gmem; };
+    std::vector<B> bins = {{1025, INT64_MAX, 512, true}, {513, 1024, 512, false},
+                           {129, 512, 256, false}, {33, 128, 128, false}, {2, 32, 32, false}};
+    int64_t stage_max = 1 << 20;
+    if (force.tri_gmem) bins = {{2, INT64_MAX, 512, true}};
+    if (force.tri_small) bins = {{2, INT64_MAX, 32, false}}, stage_max = 16;
     for (const B& bn : bins) {
       const auto r = key_range(dkeys, bn.lo, bn.hi);
       const int64_t nf = r.second - r.first;
       if (nf <= 0) continue;
       const int cap = (int)std::min<int64_t>(bn.hi, maxD);
-      const int hitcap = (int)(bn.hitcap * env_int("GD_TRI_HITS", 0) / 100);
-      const FrameLayout L = make_layout(cap, !trisum, trisum, hitcap);
+      const FrameLayout L = make_layout(cap, !trisum, trisum);
       const int* fr = tri_frames.p + r.first;
       const int64_t per_rank = (nf + world - 1) / world;
-      DBuf<char> slab;
-      int grid;
-      if (bn.gmem) {
-        grid = (int)std::min<int64_t>(per_rank, 2 * num_sms());
-        slab.alloc((size_t)grid * L.bytes, s);
-      } else {
-        grid = (int)std::min<int64_t>(per_rank, (int64_t)num_sms() * 64);
+      const size_t sm = bn.gmem ? 0 : L.bytes;
+      // persistent grid: the resident CTAs (each owns a staging list)
+      int occ = 1;
+#define GD_OCC(NTV)                                                                         \
+  {                                                                                          \
+    if (!trisum) {                                                                           \
+      set_smem(k_tri_frames<NTV>, sm);                                                       \
+      GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tri_frames<NTV>, NTV, sm)); \
+    } else {                                                                                 \
+      set_smem(k_trisum_frames<NTV>, sm);                                                    \
+      GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trisum_frames<NTV>, NTV, sm)); \
+    }                                                                                        \
+  }
+      switch (bn.nt) {
+        case 512: GD_OCC(512) break;
+        case 256: GD_OCC(256) break;
+        case 128: GD_OCC(128) break;
+        default: GD_OCC(32) break;
       }
+#undef GD_OCC
+      occ = std::max(occ, 1);
+      int grid = (int)std::min<int64_t>(per_rank, (int64_t)num_sms() * occ);
+      if (bn.gmem) grid = (int)std::min<int64_t>(per_rank, 2 * num_sms());
+      DBuf<char> slab;
+      if (bn.gmem) slab.alloc((size_t)grid * L.bytes, s);
       char* sp = bn.gmem ? slab.p : nullptr;
-      const size_t sm = sp ? 0 : L.bytes;
+      HitLists HL{};
+      DBuf<u64> stage;
+      if (lists) {
+        const int64_t c2 = (int64_t)cap * (cap - 1) / 2;
+        HL.stage_cap = (int)std::max<int64_t>(1, std::min<int64_t>(c2, stage_max));
+        if (!trisum) {
+          stage.alloc((size_t)grid * HL.stage_cap, s);
+          HL.stage = stage.p;
+        }
+        HL.buf = hit_cap ? hitbuf.p : nullptr;
+        HL.top = hittop.p;
+        HL.cap = hit_cap;
+        HL.hoff = hit_cap ? hoff.p : nullptr;
+        HL.hcnt = hit_cap ? hcnt.p : nullptr;
+      }
       for (const int rk : my_ranks) {
 #define GD_TRI_LAUNCH(NTV)                                                                   \
   if (!trisum) {                                                                             \
-    set_smem(k_tri_frames<NTV>, sm);                                                         \
     k_tri_frames<NTV><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp, OP.p, tcs.p,    \
-                                            vT.p, k4tot.p);                                  \
+                                            vT.p, k4tot.p, HL);                              \
     GD_LAUNCH_CHECK("tri_frames");                                                           \
   } else {                                                                                   \
-    set_smem(k_trisum_frames<NTV>, sm);                                                      \
     k_trisum_frames<NTV><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp, OP.p, tcs.p, \
-                                               tsl.p, tsh.p, tsd.p);                         \
+                                               tsl.p, tsh.p, tsd.p, HL);                     \
     GD_LAUNCH_CHECK("trisum_frames");                                                        \
   }
       switch (bn.nt) {
