@@ -780,6 +780,7 @@ struct RoundPlan {
   const int64_t* cpre;  // [nf+1] chunk prefix
   const int* rf;        // [R+1] round -> first frame index
   const int64_t* rch;   // [R] items per chunk of each round
+  const int* rzs;       // [R] 1: zero the round's counters by a sweep over its wedges
   int R;                // rounds
   int F;                // max frames per round (slabs per set)
   int T;                // independent teams of CTAs (round r belongs to team r % T)
@@ -854,12 +855,19 @@ k_c4_rounds(View g, const int64_t* __restrict__ WP, RoundPlan P, unsigned* __res
     unsigned* set = sets + (size_t)(it & 1) * P.F * P.slab_words;
     if (r < P.R) round_chunks<NT, kCount>(g, WP, P, r, set, tb, ts, false, c4s, c4tot2);
     if (prev >= 0) {
-      // zero the slabs of the team's previous round with wide stores
-      const int used = P.rf[prev + 1] - P.rf[prev];
-      uint4* z = (uint4*)(sets + (size_t)((it - 1) & 1) * P.F * P.slab_words);
-      const int64_t nz = (int64_t)used * P.slab_words / 4;
-      const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
-      for (int64_t i = tb * (int64_t)NT + threadIdx.x; i < nz; i += (int64_t)ts * NT) z[i] = zero4;
+      // zero the counters of the team's previous round: a sweep over its
+      // wedges when they touch few counters, else wide stores over the slabs
+      unsigned* pset = sets + (size_t)((it - 1) & 1) * P.F * P.slab_words;
+      if (P.rzs[prev]) {
+        round_chunks<NT, kZero>(g, WP, P, prev, pset, tb, ts, false, c4s, c4tot2);
+      } else {
+        const int used = P.rf[prev + 1] - P.rf[prev];
+        uint4* z = (uint4*)pset;
+        const int64_t nz = (int64_t)used * P.slab_words / 4;
+        const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
+        for (int64_t i = tb * (int64_t)NT + threadIdx.x; i < nz; i += (int64_t)ts * NT)
+          z[i] = zero4;
+      }
     }
     if (r >= P.R) break;
     team_barrier(tbar, ts, gen);
@@ -1258,7 +1266,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   // ---- pass A / pass B: triangle frames by D = |N+(a)| ----------------------
   const int64_t maxD = dkeys.empty() ? 0 : dkeys[0];
   // graph-wide hit buffer (per-edge mode): exact-size lists for pass B,
-  // capacity = min(sum_a min(items_a, C(D_a, 2)), 35% of free memory)
+  // capacity = min(sum_a min(items_a, C(D_a, 2)), 60% of free memory)
   const bool lists = env_int("GD_TRI_LISTS", 1) != 0;
   DBuf<u64> hitbuf, hittop;
   DBuf<int64_t> hoff;
@@ -1275,7 +1283,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     GD_CUDA(cudaStreamSynchronize(s));
     size_t fr = 0, tot = 0;
     GD_CUDA(cudaMemGetInfo(&fr, &tot));
-    hit_cap = std::min<u64>(hb, (u64)(fr * 0.35) / 8);
+    hit_cap = std::min<u64>(hb, (u64)(fr * 0.6) / 8);
     hit_cap = std::min<u64>(hit_cap, (u64)env_int("GD_HIT_CAP", INT64_MAX));  // tests
     if (hit_cap) {
       hitbuf.alloc(hit_cap, s);
@@ -1492,12 +1500,15 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       const int F = (int)std::max<int64_t>(
           1, std::min<int64_t>(256, l2_budget / (T * slab_words * 4)));
       // rounds of F frames; each round's chunk size gives >= 2 chunks per CTA
-      std::vector<int> rf;
+      std::vector<int> rf, rzs;
       std::vector<int64_t> rch, cpre(f16.size() + 1, 0);
       for (size_t j0 = 0; j0 < f16.size(); j0 += F) {
         const size_t j1 = std::min(f16.size(), j0 + (size_t)F);
         int64_t wr = 0;
         for (size_t j = j0; j < j1; j++) wr += w16[j];
+        // a zero sweep rewrites <= wr scattered 2-byte counters (~32 B of
+        // traffic each), a memset streams (j1-j0) slabs
+        rzs.push_back(wr * 32 < (int64_t)(j1 - j0) * slab_words * 4 ? 1 : 0);
         int64_t ch = wr / (2 * (int64_t)(grid / T));
         ch = std::max<int64_t>(1024, std::min<int64_t>(65536, (ch + 511) & ~int64_t(511)));
         rf.push_back((int)j0);
@@ -1505,11 +1516,13 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
         for (size_t j = j0; j < j1; j++) cpre[j + 1] = cpre[j] + (w16[j] + ch - 1) / ch;
       }
       rf.push_back((int)f16.size());
-      DBuf<int> dfr, drf;
+      DBuf<int> dfr, drf, drzs;
       DBuf<int64_t> dcp, drch;
       DBuf<unsigned> slabs, bar;
       dfr.alloc(f16.size(), s);
       drf.alloc(rf.size(), s);
+      drzs.alloc(rzs.size(), s);
+      GD_CUDA(cudaMemcpyAsync(drzs.p, rzs.data(), rzs.size() * 4, cudaMemcpyHostToDevice, s));
       dcp.alloc(cpre.size(), s);
       drch.alloc(rch.size(), s);
       slabs.alloc((size_t)T * 2 * F * slab_words, s);
@@ -1520,7 +1533,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       GD_CUDA(cudaMemcpyAsync(drf.p, rf.data(), rf.size() * 4, cudaMemcpyHostToDevice, s));
       GD_CUDA(cudaMemcpyAsync(dcp.p, cpre.data(), cpre.size() * 8, cudaMemcpyHostToDevice, s));
       GD_CUDA(cudaMemcpyAsync(drch.p, rch.data(), rch.size() * 8, cudaMemcpyHostToDevice, s));
-      RoundPlan P{dfr.p, dcp.p, drf.p, drch.p, (int)rf.size() - 1, F, T, slab_words};
+      RoundPlan P{dfr.p, dcp.p, drf.p, drch.p, drzs.p, (int)rf.size() - 1, F, T, slab_words};
       nrounds += P.R;
       unsigned* slabs_p = slabs.p;
       unsigned* bar_p = bar.p;
