@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -121,7 +122,20 @@ struct DevGraph {
   DBuf<int64_t> eoff;   // [G+1] canonical edge offsets per graph
   DBuf<int64_t> gn;     // [G] vertex count per graph
   std::vector<int64_t> h_eoff, h_gn;
+  // census workspace: large scratch buffers kept across calls on this graph
+  // (same sizes every call, so repeated censuses never re-allocate)
+  std::map<std::string, DBuf<char>> ws;
+  uint64_t hit_cap = 0;      // entries of the persisted hit-list buffer
+  bool hit_cap_known = false;
 };
+
+template <typename T>
+T* ws_get(DevGraph& g, const char* name, size_t count, cudaStream_t s) {
+  DBuf<char>& b = g.ws[name];
+  const size_t bytes = count * sizeof(T);
+  if (b.n < bytes) b.alloc(bytes, s);
+  return (T*)b.p;
+}
 
 // ---------------------------------------------------------------------------
 // small device helpers

@@ -73,17 +73,19 @@ typedef unsigned __int128 u128;
 struct FrameLayout {
   int cap;     // max frame size D
   int hcap;    // hash capacity (pow2 >= 2*cap)
+  int wb;      // 64-bit words per bitmap row block (column blocking of big frames)
   int rows;    // 1: pass-A bitmap rows
   int accum;   // 1: pass-B accumulators
-  size_t o_qb, o_lv, o_p, o_hk, o_hv, o_rows, o_tri2, o_tl, o_dl, o_acc;
+  size_t o_qb, o_lv, o_p, o_hk, o_hv, o_rows, o_tri2, o_dla, o_tl, o_dl, o_acc;
   size_t bytes;
 };
 
 __host__ __device__ __forceinline__ int row_stride64(int W) { return W | 1; }
 
-FrameLayout make_layout(int cap, bool rows, bool accum) {
+FrameLayout make_layout(int cap, bool rows, bool accum, int wb = 0) {
   FrameLayout L{};
   L.cap = cap;
+  L.wb = wb > 0 ? wb : (cap + 63) / 64;
   int h = 32;
   while (h < 2 * cap) h <<= 1;
   L.hcap = h;
@@ -97,15 +99,15 @@ FrameLayout make_layout(int cap, bool rows, bool accum) {
   };
   L.o_qb = take(8 * (size_t)cap);
   if (accum) L.o_acc = take(sizeof(u64) * 3 * cap);
-  if (rows) {
-    const int W = (cap + 63) / 64;
-    L.o_rows = take(8ull * cap * row_stride64(W));
-  }
+  if (rows) L.o_rows = take(8ull * cap * row_stride64(L.wb));
   L.o_lv = take(4 * (size_t)cap);
   L.o_p = take(4 * (size_t)(cap + 1));
   L.o_hk = take(4 * (size_t)h);
   L.o_hv = take(4 * (size_t)h);
-  if (rows) L.o_tri2 = take(4 * (size_t)cap);
+  if (rows) {
+    L.o_tri2 = take(4 * (size_t)cap);
+    L.o_dla = take(4 * (size_t)cap);
+  }
   if (accum) {
     L.o_tl = take(4 * (size_t)cap);
     L.o_dl = take(4 * (size_t)cap);
@@ -241,8 +243,9 @@ struct HitLists {
 // ------------------------------------------------------------------------
 // pass A
 // ------------------------------------------------------------------------
+// Frames whose bitmap rows fit in one block (all but the largest).
 template <int NT>
-__device__ void tri_frame(const View& g, int a, char* mem, const FrameLayout& L,
+__device__ void tri_frame_single(const View& g, int a, char* mem, const FrameLayout& L,
                           const int64_t* __restrict__ OP, u64* __restrict__ tcs,
                           u64* __restrict__ vT, u64* __restrict__ k4tot, const HitLists& HL) {
   __shared__ int nhits;
@@ -348,15 +351,159 @@ __device__ void tri_frame(const View& g, int a, char* mem, const FrameLayout& L,
   __syncthreads();
 }
 
+// Frames whose bitmap rows are split into column blocks (the largest).
 template <int NT>
+__device__ void tri_frame(const View& g, int a, char* mem, const FrameLayout& L,
+                          const int64_t* __restrict__ OP, u64* __restrict__ tcs,
+                          u64* __restrict__ vT, u64* __restrict__ k4tot, const HitLists& HL) {
+  __shared__ int nhits;
+  __shared__ u64 s_off;
+  LocalHash H;
+  const int D = frame_load<NT>(g, a, mem, L, OP, H);
+  const int* Lv = (const int*)(mem + L.o_lv);
+  const int* P = (const int*)(mem + L.o_p);
+  const int64_t* QB = (const int64_t*)(mem + L.o_qb);
+  u64* rows = (u64*)(mem + L.o_rows);
+  unsigned* tri2 = (unsigned*)(mem + L.o_tri2);
+  unsigned* dla = (unsigned*)(mem + L.o_dla);
+  u64* hits = HL.stage ? HL.stage + (size_t)blockIdx.x * HL.stage_cap : nullptr;
+  // bitmap rows in column blocks of WB words (one block unless D is large)
+  const int W = (D + 63) >> 6;
+  const int WB = W < L.wb ? W : L.wb;
+  const int NB = (W + WB - 1) / WB;
+  const int RS = row_stride64(WB);
+  for (int j = threadIdx.x; j < D; j += NT) {
+    tri2[j] = 0u;
+    dla[j] = 0u;
+  }
+  if (threadIdx.x == 0) nhits = 0;
+  const int total = P[D];
+  const int hitcap = (hits && D < 65536) ? HL.stage_cap : 0;
+  // set the bits of local edge (j, k) that fall in column block [c0, c1)
+  auto set_bits = [&](int j, int k, int c0, int c1) {
+    if (k >= c0 && k < c1) atomicOr(&rows[j * RS + ((k - c0) >> 6)], 1ull << ((k - c0) & 63));
+    if (j >= c0 && j < c1) atomicOr(&rows[k * RS + ((j - c0) >> 6)], 1ull << ((j - c0) & 63));
+  };
+  auto local_edge = [&](int j, int k, int64_t q, bool first) {
+    unsigned c = 0;
+    const u64* rj = rows + j * RS;
+    const u64* rk = rows + k * RS;
+    for (int w = 0; w < WB; w++) c += __popcll(rj[w] & rk[w]);
+    const u64 add = (first ? (1ull << kTriShift) : 0ull) + c;
+    if (add) atomicAdd(&tcs[q], add);
+    if (c) {
+      atomicAdd(&tri2[j], c);
+      atomicAdd(&tri2[k], c);
+    }
+  };
+  bool listed = false;
+  int nh = 0;
+  for (int blk = 0; blk < NB; blk++) {
+    const int c0 = blk * WB * 64, c1 = min(D, c0 + WB * 64);
+    const int wcnt = (c1 - c0 + 63) >> 6;  // words used in this block
+    for (int i = threadIdx.x; i < D * RS; i += NT) rows[i] = 0ull;
+    __syncthreads();
+    if (blk == 0 || !listed) {
+      // sweep 1 (probing): bitmap bits + the list of local edges
+      for_frame_items<NT>(g, P, QB, D, total, [&](int j, int i, int64_t, int y) {
+        const int k = H.find(y);
+        if (k >= 0) {
+          set_bits(j, k, c0, c1);
+          if (blk == 0 && hitcap) {  // warp-aggregated append
+            const unsigned act = __activemask();
+            const int leader = __ffs(act) - 1;
+            int h0 = 0;
+            if ((int)lane_id() == leader) h0 = atomicAdd(&nhits, __popc(act));
+            const int h = __shfl_sync(act, h0, leader) + __popc(act & ((1u << lane_id()) - 1u));
+            if (h < hitcap) hits[h] = pack_hit(j, k, i);
+          }
+        }
+      });
+      __syncthreads();
+      if (blk == 0) {
+        nh = nhits;
+        listed = hitcap > 0 && nh <= hitcap;
+        // persist the list for pass B (exact-size bump allocation)
+        if (HL.buf && threadIdx.x == 0) {
+          u64 off = ~0ull;
+          if (listed && nh > 0) {
+            off = atomicAdd(HL.top, (u64)nh);
+            if (off + (u64)nh > HL.cap) off = ~0ull;
+          }
+          s_off = off;
+          HL.hoff[a] = (int64_t)off;
+          HL.hcnt[a] = (listed && (nh == 0 || off != ~0ull)) ? nh : -1;
+        }
+        __syncthreads();
+      }
+    } else {
+      for (int h = threadIdx.x; h < nh; h += NT) {
+        const u64 e = hits[h];
+        set_bits((int)(e >> 48), (int)((e >> 32) & 0xffff), c0, c1);
+      }
+      __syncthreads();
+    }
+    // sweep 2: each local edge (x_j, x_k) is the triangle {a, x_j, x_k}; its
+    // common local neighbours are the 4-cliques {a, x_j, x_k, z}
+    if (listed) {
+      u64* dst = (blk == 0 && HL.buf && s_off != ~0ull) ? HL.buf + s_off : nullptr;
+      for (int h = threadIdx.x; h < nh; h += NT) {
+        const u64 e = hits[h];
+        if (dst) dst[h] = e;
+        const int j = (int)(e >> 48), k = (int)((e >> 32) & 0xffff), i = (int)(unsigned)e;
+        local_edge(j, k, QB[j] + i, blk == 0);
+      }
+    } else {
+      for_frame_items<NT>(g, P, QB, D, total, [&](int j, int, int64_t q, int y) {
+        const int k = H.find(y);
+        if (k >= 0) local_edge(j, k, q, blk == 0);
+      });
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < D; j += NT) {
+      unsigned dl = 0;
+      const u64* rj = rows + j * RS;
+      for (int w = 0; w < wcnt; w++) dl += __popcll(rj[w]);
+      dla[j] += dl;
+    }
+    __syncthreads();
+  }
+  const int64_t base = g.osplit[a];
+  u64 t2sum = 0, dlsum = 0;
+  for (int j = threadIdx.x; j < D; j += NT) {
+    const unsigned dl = dla[j];
+    if (dl) {
+      atomicAdd(&tcs[base + j], ((u64)dl << kTriShift) + (tri2[j] >> 1));
+      atomicAdd(&vT[Lv[j]], (u64)dl);
+    }
+    t2sum += tri2[j];
+    dlsum += dl;
+  }
+  typedef cub::BlockReduce<u64, NT> BR;
+  __shared__ typename BR::TempStorage tmp;
+  const u64 s1 = BR(tmp).Sum(t2sum);
+  __syncthreads();
+  const u64 s2 = BR(tmp).Sum(dlsum);
+  if (threadIdx.x == 0) {
+    if (s1) atomic_add_u128(k4tot + 2 * graph_of(g, a), s1 / 6);
+    if (s2) atomicAdd(&vT[a], s2 >> 1);
+  }
+  __syncthreads();
+}
+
+template <int NT, bool BLOCKED>
 __global__ void __launch_bounds__(NT)
 k_tri_frames(View g, const int* __restrict__ frames, int nframes, int rank, int world,
              FrameLayout L, char* gslab, const int64_t* __restrict__ OP, u64* __restrict__ tcs,
              u64* __restrict__ vT, u64* __restrict__ k4tot, HitLists HL) {
   extern __shared__ __align__(16) char smem[];
   char* mem = gslab ? gslab + (size_t)blockIdx.x * L.bytes : smem;
-  for (int f = rank + world * blockIdx.x; f < nframes; f += world * gridDim.x)
-    tri_frame<NT>(g, frames[f], mem, L, OP, tcs, vT, k4tot, HL);
+  for (int f = rank + world * blockIdx.x; f < nframes; f += world * gridDim.x) {
+    if (BLOCKED)
+      tri_frame<NT>(g, frames[f], mem, L, OP, tcs, vT, k4tot, HL);
+    else
+      tri_frame_single<NT>(g, frames[f], mem, L, OP, tcs, vT, k4tot, HL);
+  }
 }
 
 // ------------------------------------------------------------------------
@@ -1152,8 +1299,8 @@ void set_smem(K kernel, size_t bytes) {
 // every frame through one kernel variant so each variant can be checked
 // against the oracle on small graphs.  Results never depend on the path.
 struct ForcePaths {
-  bool tri_gmem = false, tri_small = false, c4_smem = false, c4_coop = false,
-       c4_hub32 = false;
+  bool tri_gmem = false, tri_small = false, tri_blocks = false, c4_smem = false,
+       c4_coop = false, c4_hub32 = false;
 };
 
 ForcePaths read_force() {
@@ -1163,6 +1310,7 @@ ForcePaths read_force() {
   const std::string v(e);
   f.tri_gmem = v.find("tri_gmem") != std::string::npos;
   f.tri_small = v.find("tri_small") != std::string::npos;
+  f.tri_blocks = v.find("tri_blocks") != std::string::npos;
   f.c4_smem = v.find("c4_smem") != std::string::npos;
   f.c4_coop = v.find("c4_coop") != std::string::npos;
   f.c4_hub32 = v.find("c4_hub32") != std::string::npos;
@@ -1207,30 +1355,28 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     ex.stats_names.push_back(name);
   };
 
-  // slot-indexed accumulators
-  DBuf<u64> tcs, tsl, tsh, tsd, c4s, vT, vS, k4tot, c4tot2;
-  tcs.alloc(S, s);
-  tcs.zero();
-  vT.alloc(n, s);
-  vT.zero();
-  vS.alloc(n, s);
-  k4tot.alloc(2 * G, s);
-  k4tot.zero();
-  c4tot2.alloc(2 * G, s);
-  c4tot2.zero();
+  // slot-indexed accumulators (workspace buffers, zeroed per call)
+  struct WBuf { u64* p; };
+  auto wz = [&](const char* name, size_t count) {
+    u64* q = ws_get<u64>(g, name, count, s);
+    if (count) GD_CUDA(cudaMemsetAsync(q, 0, count * 8, s));
+    return WBuf{q};
+  };
+  WBuf tcs = wz("tcs", S), vT = wz("vT", n), k4tot = wz("k4tot", 2 * G),
+       c4tot2 = wz("c4tot2", 2 * G);
+  WBuf vS{ws_get<u64>(g, "vS", n, s)};
+  WBuf tsl{nullptr}, tsh{nullptr}, tsd{nullptr}, c4s{nullptr};
   if (per_edge) {
-    for (DBuf<u64>* b : {&tsl, &tsh, &tsd, &c4s}) {
-      b->alloc(S, s);
-      b->zero();
-    }
+    tsl = wz("tsl", S);
+    tsh = wz("tsh", S);
+    tsd = wz("tsd", S);
+    c4s = wz("c4s", S);
   }
 
   // ---- schedule: item prefixes and frame orders ---------------------------
-  DBuf<int64_t> oitems, witems, OP, WP;
-  oitems.alloc(S + 1, s);
-  witems.alloc(S + 1, s);
-  OP.alloc(S + 1, s);
-  WP.alloc(S + 1, s);
+  struct IBuf { int64_t* p; };
+  IBuf oitems{ws_get<int64_t>(g, "oitems", S + 1, s)}, witems{ws_get<int64_t>(g, "witems", S + 1, s)};
+  IBuf OP{ws_get<int64_t>(g, "OP", S + 1, s)}, WP{ws_get<int64_t>(g, "WP", S + 1, s)};
   DBuf<u64> tkey, wkey, tkey_s, wkey_s;
   DBuf<int> ida, idb, tri_frames, c4_frames;
   tkey.alloc(n, s);
@@ -1246,8 +1392,6 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   }
   exclusive_scan(oitems.p, OP.p, S + 1, s);
   exclusive_scan(witems.p, WP.p, S + 1, s);
-  oitems.release();
-  witems.release();
   int64_t tot_items = 0;
   if (S) GD_CUDA(cudaMemcpyAsync(&tot_items, OP.p + S, 8, cudaMemcpyDeviceToHost, s));
   std::vector<int64_t> dkeys, wkeys;
@@ -1268,30 +1412,34 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   // graph-wide hit buffer (per-edge mode): exact-size lists for pass B,
   // capacity = min(sum_a min(items_a, C(D_a, 2)), 60% of free memory)
   const bool lists = env_int("GD_TRI_LISTS", 1) != 0;
-  DBuf<u64> hitbuf, hittop;
-  DBuf<int64_t> hoff;
-  DBuf<int> hcnt;
+  u64* hitbuf = nullptr;
+  u64* hittop = nullptr;
+  int64_t* hoff = nullptr;
+  int* hcnt = nullptr;
   u64 hit_cap = 0;
   if (per_edge && lists && n) {
-    DBuf<u64> bound;
-    bound.alloc(1, s);
-    bound.zero();
-    k_hit_bound<<<grid_cap(n, 256), 256, 0, s>>>(v, OP.p, bound.p);
-    GD_LAUNCH_CHECK("hit_bound");
-    u64 hb = 0;
-    GD_CUDA(cudaMemcpyAsync(&hb, bound.p, 8, cudaMemcpyDeviceToHost, s));
-    GD_CUDA(cudaStreamSynchronize(s));
-    size_t fr = 0, tot = 0;
-    GD_CUDA(cudaMemGetInfo(&fr, &tot));
-    hit_cap = std::min<u64>(hb, (u64)(fr * 0.6) / 8);
-    hit_cap = std::min<u64>(hit_cap, (u64)env_int("GD_HIT_CAP", INT64_MAX));  // tests
+    if (!g.hit_cap_known) {  // sized once per graph: min(bound, 40% of the device)
+      DBuf<u64> bound;
+      bound.alloc(1, s);
+      bound.zero();
+      k_hit_bound<<<grid_cap(n, 256), 256, 0, s>>>(v, OP.p, bound.p);
+      GD_LAUNCH_CHECK("hit_bound");
+      u64 hb = 0;
+      GD_CUDA(cudaMemcpyAsync(&hb, bound.p, 8, cudaMemcpyDeviceToHost, s));
+      GD_CUDA(cudaStreamSynchronize(s));
+      size_t fr = 0, tot = 0;
+      GD_CUDA(cudaMemGetInfo(&fr, &tot));
+      g.hit_cap = std::min<u64>(hb, (u64)(tot * 0.4) / 8);
+      g.hit_cap_known = true;
+    }
+    hit_cap = std::min<u64>(g.hit_cap, (u64)env_int("GD_HIT_CAP", INT64_MAX));  // tests
     if (hit_cap) {
-      hitbuf.alloc(hit_cap, s);
-      hittop.alloc(1, s);
-      hittop.zero();
-      hoff.alloc(n, s);
-      hcnt.alloc(n, s);
-      GD_CUDA(cudaMemsetAsync(hcnt.p, 0xff, n * sizeof(int), s));  // -1: not persisted
+      hitbuf = ws_get<u64>(g, "hitbuf", hit_cap, s);
+      hittop = ws_get<u64>(g, "hittop", 1, s);
+      GD_CUDA(cudaMemsetAsync(hittop, 0, 8, s));
+      hoff = ws_get<int64_t>(g, "hoff", n, s);
+      hcnt = ws_get<int>(g, "hcnt", n, s);
+      GD_CUDA(cudaMemsetAsync(hcnt, 0xff, n * sizeof(int), s));  // -1: not persisted
     }
     stat("hit_buffer_entries", (int64_t)hit_cap);
   }
@@ -1302,12 +1450,29 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     int64_t stage_max = 1 << 20;
     if (force.tri_gmem) bins = {{2, INT64_MAX, 512, true}};
     if (force.tri_small) bins = {{2, INT64_MAX, 32, false}}, stage_max = 16;
-    for (const B& bn : bins) {
+    for (B bn : bins) {
       const auto r = key_range(dkeys, bn.lo, bn.hi);
       const int64_t nf = r.second - r.first;
       if (nf <= 0) continue;
       const int cap = (int)std::min<int64_t>(bn.hi, maxD);
-      const FrameLayout L = make_layout(cap, !trisum, trisum);
+      FrameLayout L = make_layout(cap, !trisum, trisum);
+      // pass B keeps no bitmap rows: its largest frames fit shared memory;
+      // pass A splits the bitmap rows of big frames into column blocks
+      // (column blocking of pass A measured slower than global-memory rows at
+      // config 5: 309 vs 176 ms, so it is opt-in: GD_TRI_BLOCKED=1)
+      if (bn.gmem && !force.tri_gmem && (trisum || env_int("GD_TRI_BLOCKED", 0))) {
+        const int W = (cap + 63) / 64;
+        for (int nb = 1; nb <= W; nb++) {
+          FrameLayout t = make_layout(cap, !trisum, trisum, (W + nb - 1) / nb);
+          if (t.bytes <= 200 * 1024) {
+            L = t;
+            bn.gmem = false;
+            break;
+          }
+        }
+      }
+      if (force.tri_blocks && !trisum) L = make_layout(cap, true, false, 1);
+      const bool blocked = !trisum && L.wb < (cap + 63) / 64;
       const int* fr = tri_frames.p + r.first;
       const int64_t per_rank = (nf + world - 1) / world;
       const size_t sm = bn.gmem ? 0 : L.bytes;
@@ -1316,8 +1481,9 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
 #define GD_OCC(NTV)                                                                         \
   {                                                                                          \
     if (!trisum) {                                                                           \
-      set_smem(k_tri_frames<NTV>, sm);                                                       \
-      GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tri_frames<NTV>, NTV, sm)); \
+      set_smem(k_tri_frames<NTV, false>, sm);                                                \
+      set_smem(k_tri_frames<NTV, true>, sm);                                                 \
+      GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tri_frames<NTV, false>, NTV, sm)); \
     } else {                                                                                 \
       set_smem(k_trisum_frames<NTV>, sm);                                                    \
       GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trisum_frames<NTV>, NTV, sm)); \
@@ -1337,25 +1503,25 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       if (bn.gmem) slab.alloc((size_t)grid * L.bytes, s);
       char* sp = bn.gmem ? slab.p : nullptr;
       HitLists HL{};
-      DBuf<u64> stage;
       if (lists) {
         const int64_t c2 = (int64_t)cap * (cap - 1) / 2;
         HL.stage_cap = (int)std::max<int64_t>(1, std::min<int64_t>(c2, stage_max));
-        if (!trisum) {
-          stage.alloc((size_t)grid * HL.stage_cap, s);
-          HL.stage = stage.p;
-        }
-        HL.buf = hit_cap ? hitbuf.p : nullptr;
-        HL.top = hittop.p;
+        if (!trisum) HL.stage = ws_get<u64>(g, "stage", (size_t)grid * HL.stage_cap, s);
+        HL.buf = hit_cap ? hitbuf : nullptr;
+        HL.top = hittop;
         HL.cap = hit_cap;
-        HL.hoff = hit_cap ? hoff.p : nullptr;
-        HL.hcnt = hit_cap ? hcnt.p : nullptr;
+        HL.hoff = hit_cap ? hoff : nullptr;
+        HL.hcnt = hit_cap ? hcnt : nullptr;
       }
       for (const int rk : my_ranks) {
 #define GD_TRI_LAUNCH(NTV)                                                                   \
-  if (!trisum) {                                                                             \
-    k_tri_frames<NTV><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp, OP.p, tcs.p,    \
-                                            vT.p, k4tot.p, HL);                              \
+  if (!trisum && blocked) {                                                                  \
+    k_tri_frames<NTV, true><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp, OP.p,     \
+                                                  tcs.p, vT.p, k4tot.p, HL);                 \
+    GD_LAUNCH_CHECK("tri_frames_blocked");                                                   \
+  } else if (!trisum) {                                                                      \
+    k_tri_frames<NTV, false><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp, OP.p,    \
+                                                   tcs.p, vT.p, k4tot.p, HL);                \
     GD_LAUNCH_CHECK("tri_frames");                                                           \
   } else {                                                                                   \
     k_trisum_frames<NTV><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp, OP.p, tcs.p, \

@@ -60,7 +60,7 @@ def test_degenerate_graphs():
     assert np.array_equal(np.asarray(gd.micro_table(g)), np.zeros((1, 10), dtype=np.int64))
 
 
-FORCED = ["tri_gmem", "tri_small", "c4_coop", "c4_hub32", "c4_smem",
+FORCED = ["tri_gmem", "tri_small", "tri_blocks", "c4_coop", "c4_hub32", "c4_smem",
           "tri_gmem,c4_coop", "tri_small,c4_hub32"]
 
 
