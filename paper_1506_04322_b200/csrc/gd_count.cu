@@ -1251,13 +1251,67 @@ void sort_frames(u64* keys, int* ids, int64_t n, DBuf<int>& sorted_ids,
                                           0, 64, s));
 }
 
-std::vector<u64> host_keys(const DBuf<u64>& k, cudaStream_t s) {
-  std::vector<u64> raw(k.n);
-  if (k.n) GD_CUDA(cudaMemcpyAsync(raw.data(), k.p, k.n * 8, cudaMemcpyDeviceToHost, s));
-  GD_CUDA(cudaStreamSynchronize(s));
-  for (auto& x : raw) x = ~x;
-  return raw;
+// Bin boundaries of a descending key order without copying the keys: the
+// keys are stored complemented (ascending); for each threshold t the number
+// of frames with value >= t.
+__global__ void k_count_ge(const u64* __restrict__ stored, int64_t n,
+                           const u64* __restrict__ thr, int nthr, int64_t* __restrict__ out) {
+  const int t = threadIdx.x;
+  if (t >= nthr) return;
+  const u64 key = ~thr[t];
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (stored[mid] <= key) lo = mid + 1; else hi = mid;
+  }
+  out[t] = lo;
 }
+
+struct DevKeys {
+  const u64* stored = nullptr;  // complemented values, ascending
+  int64_t n = 0;
+  int shift = 0;                // value = key >> shift
+  cudaStream_t s = 0;
+  // [begin, end) of the frames with lo <= value >> shift <= hi, for all bins at once
+  std::vector<std::pair<int64_t, int64_t>> ranges(
+      const std::vector<std::pair<int64_t, int64_t>>& bins) const {
+    std::vector<u64> thr;
+    for (auto& b : bins) {
+      thr.push_back((u64)b.first << shift);
+      thr.push_back(b.second >= (INT64_MAX >> shift) ? ~0ull : (u64)(b.second + 1) << shift);
+    }
+    std::vector<int64_t> cnt(thr.size(), 0);
+    if (n && !thr.empty()) {
+      DBuf<u64> dthr;
+      DBuf<int64_t> dcnt;
+      dthr.alloc(thr.size(), s);
+      dcnt.alloc(thr.size(), s);
+      GD_CUDA(cudaMemcpyAsync(dthr.p, thr.data(), thr.size() * 8, cudaMemcpyHostToDevice, s));
+      k_count_ge<<<1, 64, 0, s>>>(stored, n, dthr.p, (int)thr.size(), dcnt.p);
+      GD_LAUNCH_CHECK("count_ge");
+      GD_CUDA(cudaMemcpyAsync(cnt.data(), dcnt.p, cnt.size() * 8, cudaMemcpyDeviceToHost, s));
+      GD_CUDA(cudaStreamSynchronize(s));
+    }
+    std::vector<std::pair<int64_t, int64_t>> out;
+    for (size_t i = 0; i < bins.size(); i++) {
+      const int64_t b = thr[2 * i + 1] == ~0ull ? 0 : cnt[2 * i + 1];
+      out.push_back({b, std::max(b, cnt[2 * i])});
+    }
+    return out;
+  }
+  // raw keys (values << shift | flags) of frames [a, b)
+  std::vector<u64> keys(int64_t a, int64_t b) const {
+    std::vector<u64> h(std::max<int64_t>(0, b - a));
+    if (!h.empty()) {
+      GD_CUDA(cudaMemcpyAsync(h.data(), stored + a, h.size() * 8, cudaMemcpyDeviceToHost, s));
+      GD_CUDA(cudaStreamSynchronize(s));
+    }
+    for (auto& x : h) x = ~x;
+    return h;
+  }
+  int64_t value(int64_t i) const { return i < n ? (int64_t)(keys(i, i + 1)[0] >> shift) : 0; }
+};
+
 
 struct Timer {
   cudaStream_t s;
@@ -1322,11 +1376,7 @@ int64_t env_int(const char* name, int64_t dflt) {
   return e ? std::atoll(e) : dflt;
 }
 
-// [begin, end) of the entries of a descending key vector with lo <= key <= hi
-std::pair<int64_t, int64_t> key_range(const std::vector<int64_t>& keys, int64_t lo, int64_t hi) {
-  auto b = std::lower_bound(keys.begin(), keys.end(), hi, std::greater<int64_t>());
-  auto e = std::upper_bound(keys.begin(), keys.end(), lo, std::greater<int64_t>());
-  return {(int64_t)(b - keys.begin()), (int64_t)(e - keys.begin())};
+
 }
 
 }  // namespace
@@ -1394,21 +1444,17 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   exclusive_scan(witems.p, WP.p, S + 1, s);
   int64_t tot_items = 0;
   if (S) GD_CUDA(cudaMemcpyAsync(&tot_items, OP.p + S, 8, cudaMemcpyDeviceToHost, s));
-  std::vector<int64_t> dkeys, wkeys;
-  std::vector<char> wbig;
+  DevKeys dk, wk;
   if (n) {
     sort_frames(tkey.p, ida.p, n, tri_frames, tkey_s, s);
     sort_frames(wkey.p, idb.p, n, c4_frames, wkey_s, s);
-    for (u64 k : host_keys(tkey_s, s)) dkeys.push_back((int64_t)k);
-    for (u64 k : host_keys(wkey_s, s)) {
-      wkeys.push_back((int64_t)(k >> 1));
-      wbig.push_back((char)(k & 1));
-    }
+    dk = DevKeys{tkey_s.p, n, 0, s};
+    wk = DevKeys{wkey_s.p, n, 1, s};
   }
   timer.mark("schedule");
 
   // ---- pass A / pass B: triangle frames by D = |N+(a)| ----------------------
-  const int64_t maxD = dkeys.empty() ? 0 : dkeys[0];
+  const int64_t maxD = n ? dk.value(0) : 0;
   // graph-wide hit buffer (per-edge mode): exact-size lists for pass B,
   // capacity = min(sum_a min(items_a, C(D_a, 2)), 60% of free memory)
   const bool lists = env_int("GD_TRI_LISTS", 1) != 0;
@@ -1450,8 +1496,12 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     int64_t stage_max = 1 << 20;
     if (force.tri_gmem) bins = {{2, INT64_MAX, 512, true}};
     if (force.tri_small) bins = {{2, INT64_MAX, 32, false}}, stage_max = 16;
-    for (B bn : bins) {
-      const auto r = key_range(dkeys, bn.lo, bn.hi);
+    std::vector<std::pair<int64_t, int64_t>> bq;
+    for (const B& bn : bins) bq.push_back({bn.lo, bn.hi});
+    const auto brs = dk.ranges(bq);
+    for (size_t bi = 0; bi < bins.size(); bi++) {
+      B bn = bins[bi];
+      const auto r = brs[bi];
       const int64_t nf = r.second - r.first;
       if (nf <= 0) continue;
       const int cap = (int)std::min<int64_t>(bn.hi, maxD);
@@ -1560,16 +1610,17 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   // with L2-resident u16 slabs; frames whose counters could exceed 16 bits
   // (lower degree >= 65536) take the u32 hub path.
   int64_t total_w = 0;
-  for (int64_t w : wkeys) total_w += w;
+  if (S) {
+    GD_CUDA(cudaMemcpyAsync(&total_w, WP.p + S, 8, cudaMemcpyDeviceToHost, s));
+    GD_CUDA(cudaStreamSynchronize(s));
+  }
   stat("wedges", total_w);
   stat("tri_items", tot_items);
   int64_t t0 = 256, t1 = 4096, t2 = 24576;
   if (force.c4_coop || force.c4_hub32) t0 = t1 = t2 = 0;
   if (force.c4_smem) t0 = t1 = 0;  // every frame <= t2 through the u16 hash
-  const auto rs0 = key_range(wkeys, 1, t0);
-  const auto rs1 = key_range(wkeys, t0 + 1, t1);
-  const auto rs2 = key_range(wkeys, t1 + 1, t2);
-  const auto rh = key_range(wkeys, t2 + 1, INT64_MAX);
+  const auto wr = wk.ranges({{1, t0}, {t0 + 1, t1}, {t1 + 1, t2}, {t2 + 1, INT64_MAX}});
+  const auto rs0 = wr[0], rs1 = wr[1], rs2 = wr[2], rh = wr[3];
   const int pe = per_edge ? 1 : 0;
   u64* c4s_p = per_edge ? c4s.p : nullptr;
   const int64_t nh = rh.second - rh.first;
@@ -1577,16 +1628,17 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   if (nh > 0) {
     std::vector<int> hf(nh);
     GD_CUDA(cudaMemcpyAsync(hf.data(), c4_frames.p + rh.first, nh * 4, cudaMemcpyDeviceToHost, s));
+    const std::vector<u64> hkeys = wk.keys(rh.first, rh.second);  // (W << 1) | big
     GD_CUDA(cudaStreamSynchronize(s));
     std::vector<int> f16_all, f32_all;
     std::vector<int64_t> w16_all, h16, h32;
     for (int64_t h = 0; h < nh; h++) {
-      if (wbig[rh.first + h] || force.c4_hub32) {
+      if ((hkeys[h] & 1) || force.c4_hub32) {
         f32_all.push_back(hf[h]);
         h32.push_back(h);
       } else {
         f16_all.push_back(hf[h]);
-        w16_all.push_back(wkeys[rh.first + h]);
+        w16_all.push_back((int64_t)(hkeys[h] >> 1));
         h16.push_back(h);
       }
     }
@@ -1759,7 +1811,8 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     // capacity > max distinct counters (<= wedges): load <= 1/2 (u32 bins)
     // or <= 3/4 (u16 bin)
     int hcap = 512;
-    while ((c16 ? 3 * (int64_t)hcap / 4 : (int64_t)hcap / 2) < wkeys[r.first]) hcap <<= 1;
+    const int64_t wmax = wk.value(r.first);
+    while ((c16 ? 3 * (int64_t)hcap / 4 : (int64_t)hcap / 2) < wmax) hcap <<= 1;
     const size_t sm = (size_t)hcap * 4 + (size_t)hcap * (c16 ? 2 : 4);
     if (sm > 200 * 1024) throw Error(GD_EINVAL, "wedge frame too large for the shared hash");
     set_smem(kernel, sm);
