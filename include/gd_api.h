@@ -127,6 +127,16 @@ GD_API int gd_sums_from_table(const int64_t* table, int64_t m, int64_t n, int fl
                        uint64_t* sums);
 
 /*
+ * Host closures for many graphs (census.py:388-430, Eqs. 1-4, Lemmas 2-8,
+ * Eqs. 18-19) in exact 128-bit integers: sums uint64 [G][13][2] ->
+ * counts int64 [G][17][2] (lo, hi of each signed 128-bit count, CLASS_IDS
+ * order); status[g] = 0 or 1 + the index of the first failing identity.
+ */
+GD_API int gd_close_counts(const uint64_t* sums, const int64_t* n_per_graph,
+                           const int64_t* m_per_graph, int64_t num_graphs, int64_t* counts,
+                           int* status);
+
+/*
  * One-shot convenience entries with the signatures a ctypes/cffi binding of
  * graphlet_census / micro_table binds (sanitized canonical edges of a
  * reference Graph: g.edges, g.m, g.n).

@@ -16,7 +16,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .census import census_batch, graphlet_census
+from .census import (_STEP_NAMES, batch_counts, census_batch, counts_as_ints,
+                     graphlet_census)
 from .classes import classes_for
 from .frequencies import GraphletFrequencies
 from .graph import GraphBatch
@@ -87,14 +88,30 @@ def feature_matrix(graphs, labels=None, config: ParallelConfig | None = None,
         t0 = time.perf_counter()
         if batch is None:
             batch = GraphBatch.from_graphs(graphs)
-        results = census_batch(batch)
+        counts, status = batch_counts(batch)
         per = (time.perf_counter() - t0) / count
-        for label, res in zip(labels, results):
-            if isinstance(res, Exception):
-                skipped.append((label, f"{type(res).__name__}: {res}"))
+        lo, hi = counts[..., 0], counts[..., 1]
+        # float(count) exactly as the reference: int64 -> float64 is correctly
+        # rounded; the rare counts beyond int64 go through Python ints
+        small = (hi == 0) & (lo >= 0)
+        fl = lo.astype(np.float64)
+        for i in range(count):
+            if status[i]:
+                skipped.append((labels[i], "ConsistencyError: " + _STEP_NAMES[int(status[i]) - 1]
+                                + " failed"))
                 continue
-            kept.append(label)
-            rows.append(_row(res, class_ids, log_scale, normalize))
+            if small[i].all():
+                row = fl[i].tolist()
+            else:
+                row = [float(v) for v in counts_as_ints(counts[i])]
+            if log_scale:
+                row = [math.log1p(v) for v in row]
+            if normalize:
+                total = sum(row)
+                if total > 0:
+                    row = [v / total for v in row]
+            kept.append(labels[i])
+            rows.append(row)
             seconds.append(per)
     else:
         graphs = list(graphs)

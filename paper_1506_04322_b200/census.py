@@ -200,23 +200,52 @@ def frequencies_from_micro(g, table: np.ndarray) -> GraphletFrequencies:
     return frequencies_from_sums(CensusSums.from_tuple(N.wide(sums)), n, m)
 
 
-def census_batch(batch: GraphBatch) -> list[GraphletFrequencies | Exception]:
-    """Global counts of every graph of a batch from one device pass.  A graph
-    whose closure fails yields its ConsistencyError in place of a result."""
+_STEP_NAMES = ("triangle closure", "2-star closure", "3-node-1-edge closure",
+               "3-node-independent closure", "4-clique closure", "chordal-cycle closure",
+               "4-cycle closure", "4-path closure", "tailed-triangle closure", "3-star closure",
+               "triangle-plus-isolated closure", "2-star-plus-isolated closure",
+               "two-edge closure", "one-edge closure", "independent closure")
+
+
+def batch_counts(batch: GraphBatch):
+    """One device census of every graph of the batch, closed in exact 128-bit
+    integers by the library: (counts int64 [G][17][2] as (lo, hi) of signed
+    128-bit values, status [G]: 0 ok, else 1 + failing closure step)."""
     G = batch.num_graphs
     sums = np.zeros(G * 2 * N.NUM_SUMS, dtype=np.uint64)
     seen = np.zeros(G, dtype=np.int64)
     N.check(N.lib().gd_census_global(batch.handle, N.ptr(sums, ctypes.c_uint64), N.ptr(seen)))
+    if not np.array_equal(seen, batch.m_per_graph):
+        bad = int(np.nonzero(seen != batch.m_per_graph)[0][0])
+        raise ConsistencyError(f"graph {bad}: processed {int(seen[bad])} edges, "
+                               f"expected {int(batch.m_per_graph[bad])}")
+    counts = np.zeros((G, 17, 2), dtype=np.int64)
+    status = np.zeros(G, dtype=np.int32)
+    N.check(N.lib().gd_close_counts(N.ptr(sums, ctypes.c_uint64), N.ptr(batch.n_per_graph),
+                                    N.ptr(batch.m_per_graph), G, N.ptr(counts),
+                                    status.ctypes.data_as(ctypes.POINTER(ctypes.c_int))))
+    return counts, status
+
+
+def counts_as_ints(counts_lohi: np.ndarray) -> list[int]:
+    lo = counts_lohi[..., 0].astype(np.uint64)
+    hi = counts_lohi[..., 1]
+    return [int(a) + (int(b) << 64) for a, b in zip(lo.tolist(), hi.tolist())]
+
+
+def census_batch(batch: GraphBatch) -> list[GraphletFrequencies | Exception]:
+    """Global counts of every graph of a batch from one device pass.  A graph
+    whose closure fails yields its ConsistencyError in place of a result."""
+    from .classes import CLASS_IDS
+    counts, status = batch_counts(batch)
     out: list = []
-    for i in range(G):
-        n, m = int(batch.n_per_graph[i]), int(batch.m_per_graph[i])
-        try:
-            if int(seen[i]) != m:
-                raise ConsistencyError(f"processed {int(seen[i])} edges, expected {m}")
-            s = N.wide(sums[i * 2 * N.NUM_SUMS:(i + 1) * 2 * N.NUM_SUMS])
-            out.append(frequencies_from_sums(CensusSums.from_tuple(s), n, m))
-        except ConsistencyError as exc:
-            out.append(exc)
+    for i in range(batch.num_graphs):
+        if status[i]:
+            out.append(ConsistencyError(_STEP_NAMES[int(status[i]) - 1] + " failed"))
+            continue
+        f = GraphletFrequencies(counts=dict(zip(CLASS_IDS, counts_as_ints(counts[i]))),
+                                n=int(batch.n_per_graph[i]), m=int(batch.m_per_graph[i]))
+        out.append(f)
     return out
 
 

@@ -435,6 +435,65 @@ int gd_census_sharded(gd_graph* h, gd_comm* c, int virtual_ranks, int per_edge, 
   });
 }
 
+// Closures of census.py:388-430 in exact 128-bit integers, for many graphs
+// at once (the batched feature path).  Each status is 0, or 1 + the index of
+// the first failing identity (a ConsistencyError in the reference).
+int gd_close_counts(const uint64_t* sums, const int64_t* n_per_graph, const int64_t* m_per_graph,
+                    int64_t num_graphs, int64_t* counts, int* status) {
+  if (!sums || !n_per_graph || !m_per_graph || !counts || !status || num_graphs < 0) {
+    t_last_error = "bad argument";
+    return GD_EINVAL;
+  }
+  typedef __int128 i128;
+  auto comb = [](i128 n, int k) -> i128 {
+    if (n < k) return 0;
+    i128 r = 1;
+    for (int i = 0; i < k; i++) r = r * (n - i) / (i + 1);
+    return r;
+  };
+  for (int64_t gi = 0; gi < num_graphs; gi++) {
+    const uint64_t* sp = sums + gi * 2 * kNumSums;
+    i128 v[kNumSums];
+    for (int k = 0; k < kNumSums; k++) v[k] = (i128)(((unsigned __int128)sp[2 * k + 1] << 64) | sp[2 * k]);
+    const i128 n = n_per_graph[gi], m = m_per_graph[gi];
+    int st = 0, step = 0;
+    auto div = [&](i128 x, int d) -> i128 {
+      step++;
+      if (st) return 0;
+      if (x % d != 0 || x < 0) st = step;
+      return x / d;
+    };
+    auto nn = [&](i128 x) -> i128 {
+      step++;
+      if (!st && x < 0) st = step;
+      return x;
+    };
+    // CensusSums.FIELDS: tri star indep3 clique4 cycle4 n_tt n_susv n_ts n_ss_same n_ti n_si n_ii outside
+    const i128 f31 = div(v[0], 3), f32 = div(v[1], 2), f33 = nn(v[2]);
+    const i128 f34 = nn(comb(n, 3) - f31 - f32 - f33);
+    const i128 f41 = div(v[3], 6);
+    const i128 f42 = nn(v[5] - 6 * f41);
+    const i128 f44 = div(v[4], 4);
+    const i128 f46 = nn(v[6] - 4 * f44);
+    const i128 f43 = div(v[7] - 4 * f42, 2);
+    const i128 f45 = div(v[8] - f43, 3);
+    const i128 f47 = div(v[9] - f43, 3);
+    const i128 f48 = div(v[10] - 2 * f46, 2);
+    const i128 f49 = div(v[12] - 6 * f41 - 4 * f42 - 2 * f43 - 4 * f44 - 2 * f46, 2);
+    const i128 f410 = nn(v[11] - 2 * f49);
+    const i128 f411 =
+        nn(comb(n, 4) - (f41 + f42 + f43 + f44 + f45 + f46 + f47 + f48 + f49 + f410));
+    const i128 out[17] = {m, comb(n, 2) - m, f31, f32, f33, f34, f41, f42, f43,
+                          f44, f45, f46, f47, f48, f49, f410, f411};
+    for (int c = 0; c < 17; c++) {
+      counts[gi * 34 + 2 * c] = (int64_t)(uint64_t)out[c];
+      counts[gi * 34 + 2 * c + 1] = (int64_t)(out[c] >> 64);
+    }
+    status[gi] = st;
+  }
+  return GD_OK;
+}
+
 int gd_graph_timings(const gd_graph* h, float* ms, int capacity, const char** names) {
   if (!h) return 0;
   int k = (int)std::min<size_t>(h->ms.size(), (size_t)std::max(capacity, 0));

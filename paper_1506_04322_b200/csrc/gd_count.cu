@@ -1376,9 +1376,6 @@ int64_t env_int(const char* name, int64_t dflt) {
   return e ? std::atoll(e) : dflt;
 }
 
-
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------------------

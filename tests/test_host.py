@@ -119,3 +119,34 @@ def test_product_does_not_import_oracle():
     for p in pkg.rglob("*.py"):
         txt = p.read_text()
         assert "import oracle" not in txt and "from oracle" not in txt, p
+
+
+def test_library_closures_match_python_closures():
+    """gd_close_counts (exact 128-bit closures for batches) == the Python-int
+    closures, and flags the same failing identities."""
+    import ctypes
+    from paper_1506_04322_b200.census import counts_as_ints
+    cases = small_graphs()
+    G = len(cases)
+    sums = np.zeros((G, 13, 2), dtype=np.uint64)
+    ns = np.zeros(G, dtype=np.int64)
+    ms = np.zeros(G, dtype=np.int64)
+    for i, (name, n, edges, counts, micro) in enumerate(cases):
+        for k, v in enumerate(O.sums_from_rows(micro, n, len(edges))):
+            sums[i, k] = (v & ((1 << 64) - 1), v >> 64)
+        ns[i], ms[i] = n, len(edges)
+    bad = sums.copy()
+    bad[0, 0, 0] += 1  # triangle total not divisible by 3
+    L = N.load_library()
+    for arr, expect_bad in ((sums, False), (bad, True)):
+        out = np.zeros((G, 17, 2), dtype=np.int64)
+        st = np.zeros(G, dtype=np.int32)
+        N.check(L.gd_close_counts(N.ptr(np.ascontiguousarray(arr), ctypes.c_uint64), N.ptr(ns),
+                                  N.ptr(ms), G, N.ptr(out),
+                                  st.ctypes.data_as(ctypes.POINTER(ctypes.c_int))))
+        for i, (name, n, edges, counts, micro) in enumerate(cases):
+            if expect_bad and i == 0:
+                assert st[0] == 1  # first identity: triangle closure
+                continue
+            assert st[i] == 0, name
+            assert counts_as_ints(out[i]) == [counts[c] for c in gd.CLASS_IDS], name
