@@ -346,6 +346,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(raw, args.mode, args.cpu_budget)
 
+    batch = None
+    if rank == 0 and args.batch:
+        batch = bench_batch(gd, N, L, with_cpu=world == 1 and not args.no_cpu_baseline)
+
     # secondary: the global-only census on the same resident graph
     glob = None
     if per_edge and args.global_too:
@@ -390,6 +394,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "clocks": clk,
             "cpu_baseline": cpu,
             "global_mode": glob,
+            "batch_c4": batch,
             "counts": {"g3_1": str(f_ref.counts["g3_1"]), "g4_1": str(f_ref.counts["g4_1"]),
                        "g4_4": str(f_ref.counts["g4_4"])},
         }
@@ -400,6 +405,41 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         comm.close()
     dist.close()
     return 0
+
+
+def bench_batch(gd, N, L, with_cpu: bool) -> dict:
+    """Config 4: 4,096 small graphs -> 17-count feature rows (feature_matrix),
+    end to end from host pairs (one batched device pass)."""
+    from paper_1506_04322_b200 import workloads as W
+    raws = W.config_batch()
+    pairs = [r.pairs for r in raws]
+    ns = [r.n for r in raws]
+    times, dev = [], []
+    for i in range(4):
+        L.gd_flush_l2()
+        t0 = time.perf_counter()
+        b = gd.GraphBatch(pairs, ns)
+        fm = gd.feature_matrix(b)
+        dt = time.perf_counter() - t0
+        if i:
+            times.append(dt)
+            dev.append(sum(gd.last_timings(b).values()))
+    m = int(b.m_per_graph.sum())
+    out = {"graphs": len(raws), "sum_m": m, "e2e_ms": statistics.median(times) * 1e3,
+           "device_census_ms": statistics.median(dev),
+           "e2e_edges_per_s": m / statistics.median(times),
+           "graphs_per_s": len(raws) / statistics.median(times), "skipped": len(fm.skipped)}
+    if with_cpu:
+        from oracle import oracle as O
+        idx = np.random.default_rng(3).choice(len(raws), 256, replace=False)
+        t0 = time.perf_counter()
+        for i in idx:
+            O.census(O.canonical_edges(raws[i].pairs), raws[i].n, threads=1)
+        t = (time.perf_counter() - t0) * len(raws) / len(idx)
+        out["cpu_baseline"] = {"value": m / t, "unit": "edges/s", "cores": 1, "kind": "port",
+                               "sample": "256 of the 4096 graphs, serial (the reference loops "
+                                         "graphs serially in feature_matrix), extrapolated"}
+    return out
 
 
 def main():
@@ -414,6 +454,8 @@ def main():
                     help="seconds of CPU work per baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-global", dest="global_too", action="store_false")
+    ap.add_argument("--no-batch", dest="batch", action="store_false",
+                    help="skip the config-4 batch (feature_matrix) measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -186,6 +186,11 @@ def _big_parity(name, sample):
     gold = configs().get(name)
     if gold and "counts" in gold:
         assert f.counts == int_counts(gold["counts"])
+    full = GOLDEN / f"oracle_{name}.json"  # full census by the C oracle (tools/)
+    if full.exists():
+        import json
+        d = json.loads(full.read_text())
+        assert d["m"] == g.m and f.counts == int_counts(d["counts"])
     return g, f
 
 
