@@ -316,6 +316,24 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     ms = dist.max(statistics.mean(step_ms))
     stats = gd.last_stats(g)
 
+    # secondary: the global-only census on the same resident graph
+    glob = None
+    if per_edge and args.global_too:
+        gms = []
+        for i in range(3):
+            L.gd_flush_l2()
+            fg = census_global(g)
+            if i:
+                gms.append(sum(gd.last_timings(g).values()))
+        if fg != f_ref:
+            raise SystemExit("global census differs from per-edge census")
+        gm = dist.max(statistics.mean(gms))
+        glob = {"ms_per_step": gm, "value": m / (gm / 1e3), "unit": "edges/s"}
+
+    # the resident graph (and its census workspace) is released before the
+    # end-to-end runs, which build their own device graph every step
+    deg = np.asarray(g.degrees, dtype=np.int64)
+    del g
     # --- end to end through the public API (host memory both ways) ----------
     dist.barrier()
     e2e_ms = []
@@ -333,7 +351,6 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     e2e = dist.max(statistics.mean(e2e_ms))
 
     # --- roofline: SURVEY 8(d) algorithmic bytes of one census ---------------
-    deg = np.asarray(g.degrees, dtype=np.int64)
     sum_d2 = int(np.dot(deg, deg))
     o_bytes, k_out = 8, (10 if per_edge else 0)
     b_alg = m * (8 + 4 * o_bytes + 8 * k_out) + 4 * sum_d2
@@ -349,20 +366,6 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     batch = None
     if rank == 0 and args.batch:
         batch = bench_batch(gd, N, L, with_cpu=world == 1 and not args.no_cpu_baseline)
-
-    # secondary: the global-only census on the same resident graph
-    glob = None
-    if per_edge and args.global_too:
-        gms = []
-        for i in range(3):
-            L.gd_flush_l2()
-            fg = census_global(g)
-            if i:
-                gms.append(sum(gd.last_timings(g).values()))
-        if fg != f_ref:
-            raise SystemExit("global census differs from per-edge census")
-        gm = dist.max(statistics.mean(gms))
-        glob = {"ms_per_step": gm, "value": m / (gm / 1e3), "unit": "edges/s"}
 
     if rank == 0:
         line = {
