@@ -928,6 +928,7 @@ struct RoundPlan {
   const int* rf;        // [R+1] round -> first frame index
   const int64_t* rch;   // [R] items per chunk of each round
   const int* rzs;       // [R] 1: zero the round's counters by a sweep over its wedges
+  const int* rscan;     // [R] 1 (global mode): sums and zeroing by a scan of the slabs
   int R;                // rounds
   int F;                // max frames per round (slabs per set)
   int T;                // independent teams of CTAs (round r belongs to team r % T)
@@ -998,17 +999,42 @@ k_c4_rounds(View g, const int64_t* __restrict__ WP, RoundPlan P, unsigned* __res
   unsigned* sets = slabs + (size_t)team * 2 * P.F * P.slab_words;
   unsigned gen = 0;
   int prev = -1, it = 0;
+  bool prev_scan = false;
+  typedef cub::BlockReduce<u64, NT> BR;
+  __shared__ typename BR::TempStorage tmp;
   for (int r = team; ; r += P.T, it++) {
     unsigned* set = sets + (size_t)(it & 1) * P.F * P.slab_words;
     if (r < P.R) round_chunks<NT, kCount>(g, WP, P, r, set, tb, ts, false, c4s, c4tot2);
     if (prev >= 0) {
-      // zero the counters of the team's previous round: a sweep over its
-      // wedges when they touch few counters, else wide stores over the slabs
       unsigned* pset = sets + (size_t)((it - 1) & 1) * P.F * P.slab_words;
-      if (P.rzs[prev]) {
+      const int f0 = P.rf[prev], used = P.rf[prev + 1] - f0;
+      if (prev_scan) {
+        // global mode, wedge-heavy round: 2*C(c,2) straight from the counter
+        // slabs (a sequential scan, far shorter than the wedge list), zeroing
+        // them on the way
+        for (int fj = 0; fj < used; fj++) {
+          uint4* z = (uint4*)(pset + (size_t)fj * P.slab_words);
+          u64 local = 0;
+          for (int64_t i = tb * (int64_t)NT + threadIdx.x; i < P.slab_words / 4;
+               i += (int64_t)ts * NT) {
+            const uint4 w4 = z[i];
+            const unsigned wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+              const u64 c0 = wv[t] & 0xffffu, c1 = wv[t] >> 16;
+              local += c0 * (c0 - (c0 > 0)) + c1 * (c1 - (c1 > 0));
+            }
+            if (wv[0] | wv[1] | wv[2] | wv[3]) z[i] = make_uint4(0u, 0u, 0u, 0u);
+          }
+          const u64 sum = BR(tmp).Sum(local);
+          if (threadIdx.x == 0 && sum)
+            atomic_add_u128(c4tot2 + 2 * graph_of(g, P.frames[f0 + fj]), sum);
+          __syncthreads();
+        }
+      } else if (P.rzs[prev]) {
+        // zero by a sweep over the round's wedges when they touch few counters
         round_chunks<NT, kZero>(g, WP, P, prev, pset, tb, ts, false, c4s, c4tot2);
       } else {
-        const int used = P.rf[prev + 1] - P.rf[prev];
         uint4* z = (uint4*)pset;
         const int64_t nz = (int64_t)used * P.slab_words / 4;
         const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
@@ -1018,8 +1044,11 @@ k_c4_rounds(View g, const int64_t* __restrict__ WP, RoundPlan P, unsigned* __res
     }
     if (r >= P.R) break;
     team_barrier(tbar, ts, gen);
-    round_chunks<NT, kUse>(g, WP, P, r, set, tb, ts, per_edge != 0, c4s, c4tot2);
-    team_barrier(tbar, ts, gen);
+    prev_scan = !per_edge && P.rscan[r];
+    if (!prev_scan) {
+      round_chunks<NT, kUse>(g, WP, P, r, set, tb, ts, per_edge != 0, c4s, c4tot2);
+      team_barrier(tbar, ts, gen);
+    }
     prev = r;
   }
 }
@@ -1715,7 +1744,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       const int F = (int)std::max<int64_t>(
           1, std::min<int64_t>(256, l2_budget / (T * slab_words * 4)));
       // rounds of F frames; each round's chunk size gives >= 2 chunks per CTA
-      std::vector<int> rf, rzs;
+      std::vector<int> rf, rzs, rscan;
       std::vector<int64_t> rch, cpre(f16.size() + 1, 0);
       for (size_t j0 = 0; j0 < f16.size(); j0 += F) {
         const size_t j1 = std::min(f16.size(), j0 + (size_t)F);
@@ -1724,6 +1753,9 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
         // a zero sweep rewrites <= wr scattered 2-byte counters (~32 B of
         // traffic each), a memset streams (j1-j0) slabs
         rzs.push_back(wr * 32 < (int64_t)(j1 - j0) * slab_words * 4 ? 1 : 0);
+        // a slab scan reads 4 B per counter pair sequentially, the use sweep
+        // ~32 B per wedge scattered
+        rscan.push_back(wr * 32 > (int64_t)(j1 - j0) * slab_words * 4 * 2 ? 1 : 0);
         int64_t ch = wr / (2 * (int64_t)(grid / T));
         ch = std::max<int64_t>(1024, std::min<int64_t>(65536, (ch + 511) & ~int64_t(511)));
         rf.push_back((int)j0);
@@ -1731,13 +1763,16 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
         for (size_t j = j0; j < j1; j++) cpre[j + 1] = cpre[j] + (w16[j] + ch - 1) / ch;
       }
       rf.push_back((int)f16.size());
-      DBuf<int> dfr, drf, drzs;
+      DBuf<int> dfr, drf, drzs, drscan;
       DBuf<int64_t> dcp, drch;
       DBuf<unsigned> slabs, bar;
       dfr.alloc(f16.size(), s);
       drf.alloc(rf.size(), s);
       drzs.alloc(rzs.size(), s);
       GD_CUDA(cudaMemcpyAsync(drzs.p, rzs.data(), rzs.size() * 4, cudaMemcpyHostToDevice, s));
+      drscan.alloc(rscan.size(), s);
+      GD_CUDA(cudaMemcpyAsync(drscan.p, rscan.data(), rscan.size() * 4, cudaMemcpyHostToDevice,
+                              s));
       dcp.alloc(cpre.size(), s);
       drch.alloc(rch.size(), s);
       slabs.alloc((size_t)T * 2 * F * slab_words, s);
@@ -1748,7 +1783,8 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       GD_CUDA(cudaMemcpyAsync(drf.p, rf.data(), rf.size() * 4, cudaMemcpyHostToDevice, s));
       GD_CUDA(cudaMemcpyAsync(dcp.p, cpre.data(), cpre.size() * 8, cudaMemcpyHostToDevice, s));
       GD_CUDA(cudaMemcpyAsync(drch.p, rch.data(), rch.size() * 8, cudaMemcpyHostToDevice, s));
-      RoundPlan P{dfr.p, dcp.p, drf.p, drch.p, drzs.p, (int)rf.size() - 1, F, T, slab_words};
+      RoundPlan P{dfr.p, dcp.p, drf.p, drch.p, drzs.p, drscan.p, (int)rf.size() - 1, F, T,
+                  slab_words};
       nrounds += P.R;
       unsigned* slabs_p = slabs.p;
       unsigned* bar_p = bar.p;
