@@ -220,6 +220,12 @@ __device__ __forceinline__ void for_frame_items(const View& g, const int* P, con
   }
 }
 
+// Set bit b of a 64-bit-word bitmap row with a native 32-bit atomicOr (a
+// 64-bit shared-memory atomicOr compiles to a CAS loop).
+__device__ __forceinline__ void set_bit(u64* row, int b) {
+  atomicOr((unsigned*)row + (b >> 5), 1u << (b & 31));
+}
+
 __device__ __forceinline__ u64 pack_hit(int j, int k, int i) {
   return ((u64)(unsigned)j << 48) | ((u64)(unsigned)k << 32) | (u64)(unsigned)i;
 }
@@ -270,8 +276,8 @@ __device__ void tri_frame_single(const View& g, int a, char* mem, const FrameLay
   for_frame_items<NT>(g, P, QB, D, total, [&](int j, int i, int64_t, int y) {
     const int k = H.find(y);
     if (k >= 0) {
-      atomicOr(&rows[j * RS + (k >> 6)], 1ull << (k & 63));
-      atomicOr(&rows[k * RS + (j >> 6)], 1ull << (j & 63));
+      set_bit(rows + j * RS, k);
+      set_bit(rows + k * RS, j);
       if (hitcap) {  // warp-aggregated append
         const unsigned act = __activemask();
         const int leader = __ffs(act) - 1;
@@ -381,8 +387,8 @@ __device__ void tri_frame(const View& g, int a, char* mem, const FrameLayout& L,
   const int hitcap = (hits && D < 65536) ? HL.stage_cap : 0;
   // set the bits of local edge (j, k) that fall in column block [c0, c1)
   auto set_bits = [&](int j, int k, int c0, int c1) {
-    if (k >= c0 && k < c1) atomicOr(&rows[j * RS + ((k - c0) >> 6)], 1ull << ((k - c0) & 63));
-    if (j >= c0 && j < c1) atomicOr(&rows[k * RS + ((j - c0) >> 6)], 1ull << ((j - c0) & 63));
+    if (k >= c0 && k < c1) set_bit(rows + j * RS, k - c0);
+    if (j >= c0 && j < c1) set_bit(rows + k * RS, j - c0);
   };
   auto local_edge = [&](int j, int k, int64_t q, bool first) {
     unsigned c = 0;
@@ -491,13 +497,16 @@ __device__ void tri_frame(const View& g, int a, char* mem, const FrameLayout& L,
   __syncthreads();
 }
 
-template <int NT, bool BLOCKED>
+// GM: frame scratch in a global slab (largest frames); otherwise in shared
+// memory, where keeping the pointer's provenance static lets the compiler
+// emit LDS/STS/ATOMS instead of generic loads.
+template <int NT, bool BLOCKED, bool GM>
 __global__ void __launch_bounds__(NT)
 k_tri_frames(View g, const int* __restrict__ frames, int nframes, int rank, int world,
              FrameLayout L, char* gslab, const int64_t* __restrict__ OP, u64* __restrict__ tcs,
              u64* __restrict__ vT, u64* __restrict__ k4tot, HitLists HL) {
   extern __shared__ __align__(16) char smem[];
-  char* mem = gslab ? gslab + (size_t)blockIdx.x * L.bytes : smem;
+  char* mem = GM ? gslab + (size_t)blockIdx.x * L.bytes : smem;
   for (int f = rank + world * blockIdx.x; f < nframes; f += world * gridDim.x) {
     if (BLOCKED)
       tri_frame<NT>(g, frames[f], mem, L, OP, tcs, vT, k4tot, HL);
@@ -511,7 +520,10 @@ k_tri_frames(View g, const int* __restrict__ frames, int nframes, int rank, int 
 //   tsl: sum t(lo, w)   tsh: sum t(hi, w)   tsd: sum d(w)   (w in Tri_e)
 // Frames with a persisted hit list walk it; the others probe again.
 // ------------------------------------------------------------------------
-template <int NT>
+// AccT: the per-base-edge accumulators in shared memory; u32 when
+// D * max_degree < 2^32 (native shared atomics; a 64-bit shared atomicAdd is
+// a CAS loop), u64 otherwise.
+template <int NT, typename AccT>
 __device__ void trisum_frame(const View& g, int a, char* mem, const FrameLayout& L,
                              const int64_t* __restrict__ OP, const u64* __restrict__ tcs,
                              u64* __restrict__ tsl, u64* __restrict__ tsh,
@@ -523,7 +535,7 @@ __device__ void trisum_frame(const View& g, int a, char* mem, const FrameLayout&
   const int64_t* QB = (const int64_t*)(mem + L.o_qb);
   int* tL = (int*)(mem + L.o_tl);
   int* dL = (int*)(mem + L.o_dl);
-  u64* acc = (u64*)(mem + L.o_acc);
+  AccT* acc = (AccT*)(mem + L.o_acc);
   const int64_t base = g.osplit[a];
   for (int j = threadIdx.x; j < D; j += NT) {
     tL[j] = (int)(tcs[base + j] >> kTriShift);
@@ -542,12 +554,12 @@ __device__ void trisum_frame(const View& g, int a, char* mem, const FrameLayout&
     atomicAdd(&tsh[q], (u64)tL[k]);
     atomicAdd(&tsd[q], deg_a);
     // edge (a, x_j): third vertex x_k; edge (a, x_k): third vertex x_j
-    atomicAdd(&acc[3 * j], (u64)tL[k]);
-    atomicAdd(&acc[3 * j + 1], t_jk);
-    atomicAdd(&acc[3 * j + 2], (u64)dL[k]);
-    atomicAdd(&acc[3 * k], (u64)tL[j]);
-    atomicAdd(&acc[3 * k + 1], t_jk);
-    atomicAdd(&acc[3 * k + 2], (u64)dL[j]);
+    atomicAdd(&acc[3 * j], (AccT)tL[k]);
+    atomicAdd(&acc[3 * j + 1], (AccT)t_jk);
+    atomicAdd(&acc[3 * j + 2], (AccT)dL[k]);
+    atomicAdd(&acc[3 * k], (AccT)tL[j]);
+    atomicAdd(&acc[3 * k + 1], (AccT)t_jk);
+    atomicAdd(&acc[3 * k + 2], (AccT)dL[j]);
   };
   const int nh = HL.hcnt ? HL.hcnt[a] : -1;
   if (nh >= 0) {
@@ -566,23 +578,23 @@ __device__ void trisum_frame(const View& g, int a, char* mem, const FrameLayout&
   __syncthreads();
   for (int j = threadIdx.x; j < D; j += NT) {
     if (acc[3 * j + 2] == 0) continue;  // no triangle on edge (a, x_j)
-    atomicAdd(&tsl[base + j], acc[3 * j]);
-    atomicAdd(&tsh[base + j], acc[3 * j + 1]);
-    atomicAdd(&tsd[base + j], acc[3 * j + 2]);
+    atomicAdd(&tsl[base + j], (u64)acc[3 * j]);
+    atomicAdd(&tsh[base + j], (u64)acc[3 * j + 1]);
+    atomicAdd(&tsd[base + j], (u64)acc[3 * j + 2]);
   }
   __syncthreads();
 }
 
-template <int NT>
+template <int NT, bool GM, typename AccT>
 __global__ void __launch_bounds__(NT)
 k_trisum_frames(View g, const int* __restrict__ frames, int nframes, int rank, int world,
                 FrameLayout L, char* gslab, const int64_t* __restrict__ OP,
                 const u64* __restrict__ tcs, u64* __restrict__ tsl, u64* __restrict__ tsh,
                 u64* __restrict__ tsd, HitLists HL) {
   extern __shared__ __align__(16) char smem[];
-  char* mem = gslab ? gslab + (size_t)blockIdx.x * L.bytes : smem;
+  char* mem = GM ? gslab + (size_t)blockIdx.x * L.bytes : smem;
   for (int f = rank + world * blockIdx.x; f < nframes; f += world * gridDim.x)
-    trisum_frame<NT>(g, frames[f], mem, L, OP, tcs, tsl, tsh, tsd, HL);
+    trisum_frame<NT, AccT>(g, frames[f], mem, L, OP, tcs, tsl, tsh, tsd, HL);
 }
 
 // Upper bound of the local-edge count of all frames: sum_a min(items_a, C(D_a, 2)).
@@ -1549,6 +1561,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       }
       if (force.tri_blocks && !trisum) L = make_layout(cap, true, false, 1);
       const bool blocked = !trisum && L.wb < (cap + 63) / 64;
+      const bool acc32 = (int64_t)cap * g.max_deg < (int64_t)UINT32_MAX;
       const int* fr = tri_frames.p + r.first;
       const int64_t per_rank = (nf + world - 1) / world;
       const size_t sm = bn.gmem ? 0 : L.bytes;
@@ -1557,12 +1570,13 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
 #define GD_OCC(NTV)                                                                         \
   {                                                                                          \
     if (!trisum) {                                                                           \
-      set_smem(k_tri_frames<NTV, false>, sm);                                                \
-      set_smem(k_tri_frames<NTV, true>, sm);                                                 \
-      GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tri_frames<NTV, false>, NTV, sm)); \
+      set_smem(k_tri_frames<NTV, false, false>, sm);                                         \
+      set_smem(k_tri_frames<NTV, true, false>, sm);                                          \
+      GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tri_frames<NTV, false, false>, NTV, sm)); \
     } else {                                                                                 \
-      set_smem(k_trisum_frames<NTV>, sm);                                                    \
-      GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trisum_frames<NTV>, NTV, sm)); \
+      set_smem(k_trisum_frames<NTV, false, unsigned>, sm);                                   \
+      set_smem(k_trisum_frames<NTV, false, u64>, sm);                                        \
+      GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trisum_frames<NTV, false, u64>, NTV, sm)); \
     }                                                                                        \
   }
       switch (bn.nt) {
@@ -1592,16 +1606,33 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       for (const int rk : my_ranks) {
 #define GD_TRI_LAUNCH(NTV)                                                                   \
   if (!trisum && blocked) {                                                                  \
-    k_tri_frames<NTV, true><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp, OP.p,     \
-                                                  tcs.p, vT.p, k4tot.p, HL);                 \
+    if (sp)                                                                                  \
+      k_tri_frames<NTV, true, true><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp,   \
+                                                          OP.p, tcs.p, vT.p, k4tot.p, HL);    \
+    else                                                                                     \
+      k_tri_frames<NTV, true, false><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp,  \
+                                                           OP.p, tcs.p, vT.p, k4tot.p, HL);   \
     GD_LAUNCH_CHECK("tri_frames_blocked");                                                   \
   } else if (!trisum) {                                                                      \
-    k_tri_frames<NTV, false><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp, OP.p,    \
-                                                   tcs.p, vT.p, k4tot.p, HL);                \
+    if (sp)                                                                                  \
+      k_tri_frames<NTV, false, true><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp,  \
+                                                           OP.p, tcs.p, vT.p, k4tot.p, HL);   \
+    else                                                                                     \
+      k_tri_frames<NTV, false, false><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp, \
+                                                            OP.p, tcs.p, vT.p, k4tot.p, HL);  \
     GD_LAUNCH_CHECK("tri_frames");                                                           \
   } else {                                                                                   \
-    k_trisum_frames<NTV><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp, OP.p, tcs.p, \
-                                               tsl.p, tsh.p, tsd.p, HL);                     \
+    if (sp)                                                                                  \
+      k_trisum_frames<NTV, true, u64><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp,  \
+                                                            OP.p, tcs.p, tsl.p, tsh.p, tsd.p, \
+                                                            HL);                               \
+    else if (acc32)                                                                          \
+      k_trisum_frames<NTV, false, unsigned><<<grid, NTV, sm, s>>>(                            \
+          v, fr, (int)nf, rk, world, L, sp, OP.p, tcs.p, tsl.p, tsh.p, tsd.p, HL);           \
+    else                                                                                     \
+      k_trisum_frames<NTV, false, u64><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp, \
+                                                             OP.p, tcs.p, tsl.p, tsh.p,      \
+                                                             tsd.p, HL);                     \
     GD_LAUNCH_CHECK("trisum_frames");                                                        \
   }
       switch (bn.nt) {
