@@ -1771,7 +1771,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       const int grid = per_sm * num_sms();
       const int64_t slab_words = (((n + 1) / 2) + 31) & ~int64_t(31);  // multiple of 4
       const int T = (int)std::max<int64_t>(1, std::min<int64_t>(grid, env_int("GD_C4_TEAMS", 4)));
-      const int64_t l2_budget = env_int("GD_C4_L2_MB", 128) << 20;  // all teams, one set each
+      const int64_t l2_budget = env_int("GD_C4_L2_MB", 256) << 20;  // all teams, one set each
       const int F = (int)std::max<int64_t>(
           1, std::min<int64_t>(256, l2_budget / (T * slab_words * 4)));
       // rounds of F frames; each round's chunk size gives >= 2 chunks per CTA
