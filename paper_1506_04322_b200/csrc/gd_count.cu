@@ -663,8 +663,6 @@ __device__ __forceinline__ int64_t wedge_slot(const int64_t* __restrict__ WP, in
   return lo;
 }
 
-constexpr int kWedgeK = 16;
-
 enum WedgeMode { kCount = 0, kUse = 1, kZero = 2, kTake = 3 };
 
 struct SlabCounter {  // dense u32 counters in global memory
@@ -716,79 +714,76 @@ struct HashCounter {  // shared-memory open-addressing hash, u32 or u16 counts
 };
 
 // One sweep of `mode` over items [i0, i1) of frame s (lower slots [b, o)).
-// Warp chunks of 32*K consecutive items; lane l handles c0+l, c0+l+32, ...,
-// so lanes read consecutive entries of one row w (coalesced) and the slot of
-// an item is found by one binary search per lane per chunk.  Returns the
-// thread's partial (kUse: sum of cnt-1; kTake: sum of c*(c-1)).
-template <int NT, int MODE, typename C>
-__device__ u64 wedge_sweep(const View& g, const int64_t* __restrict__ WP, int64_t b, int64_t o,
-                           int64_t i0, int64_t i1, const C& ctr, bool per_edge,
-                           u64* __restrict__ c4s) {
-  constexpr int U = 1;  // items per lane in flight (U > 1 measured slower)
+// Each warp takes one contiguous piece (a multiple of 32 items); lane l
+// handles c0+l, c0+l+32, ..., so lanes read consecutive entries of one row w
+// (coalesced).  The slot of the first item is found by one binary search per
+// lane per piece; later rows follow by advancing p (measured: per-512-item
+// searches spent ~40% of the heavy-frame kernel's stalls on that chain).
+// Returns the thread's partial (kUse: sum of cnt-1; kTake: sum of c*(c-1)).
+template <int NT, int MODE, typename C, int U = 1>
+__device__ __forceinline__ u64 wedge_sweep(const View& g, const int64_t* __restrict__ WP,
+                                           int64_t b, int64_t o, int64_t i0, int64_t i1,
+                                           const C& ctr, bool per_edge, u64* __restrict__ c4s) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int nw = NT / 32;
-  constexpr int64_t CH = 32 * kWedgeK;
+  const int64_t per = (((i1 - i0) + nw - 1) / nw + 31) & ~int64_t(31);
+  const int64_t c0 = i0 + (int64_t)warp * per;
+  const int64_t c1 = c0 + per < i1 ? c0 + per : i1;
+  int64_t i = c0 + lane;
   u64 local = 0;
-  for (int64_t c0 = i0 + (int64_t)warp * CH; c0 < i1; c0 += (int64_t)nw * CH) {
-    const int64_t c1 = c0 + CH < i1 ? c0 + CH : i1;
-    int64_t i = c0 + lane;
-    if (i >= c1) continue;
-    int64_t p = wedge_slot(WP, b, o, i);
-    int64_t wp1 = WP[p + 1];
-    int64_t base = g.rp[g.col[p]] - WP[p];  // slot of item i in row w: base + i
-    int64_t ptop = p;                       // per-edge: pending sum for slot ptop (edge s-w)
-    u64 top = 0;
-    for (; i < c1; i += 32 * U) {
-      int64_t pp[U], qq[U];
-      int xx[U];
+  if (i >= c1) return 0;
+  int64_t p = wedge_slot(WP, b, o, i);
+  int64_t wp1 = WP[p + 1];
+  int64_t base = g.rp[g.col[p]] - WP[p];  // slot of item i in row w: base + i
+  int64_t ptop = p;                       // per-edge: pending sum for slot ptop (edge s-w)
+  u64 top = 0;
+  for (; i < c1; i += 32 * U) {
+    int64_t qq[U], pp[U];
+    int xx[U];
 #pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int64_t ii = i + 32 * u;
-        if (ii < c1) {
-          if (wp1 <= ii) {
-            do {
-              p++;
-              wp1 = WP[p + 1];
-            } while (wp1 <= ii);
-            base = g.rp[g.col[p]] - WP[p];
-          }
-          pp[u] = p;
-          qq[u] = base + ii;
-        }
+    for (int u = 0; u < U; u++) {  // U items in flight per lane
+      const int64_t ii = i + 32 * u;
+      if (ii < c1 && wp1 <= ii) {
+        do {
+          p++;
+          wp1 = WP[p + 1];
+        } while (wp1 <= ii);
+        base = g.rp[g.col[p]] - WP[p];
       }
+      qq[u] = base + ii;
+      pp[u] = p;
+    }
 #pragma unroll
-      for (int u = 0; u < U; u++)
-        if (i + 32 * u < c1) xx[u] = __ldg(g.col + qq[u]);
+    for (int u = 0; u < U; u++) xx[u] = i + 32 * u < c1 ? __ldg(g.col + qq[u]) : 0;
 #pragma unroll
-      for (int u = 0; u < U; u++) {
-        if (i + 32 * u >= c1) break;
-        const int x = xx[u];
-        if (MODE == kCount) {
-          ctr.inc(x);
-        } else if (MODE == kZero) {
-          ctr.zero(x);
-        } else if (MODE == kTake) {
-          const u64 c = ctr.take(x);
-          local += c * (c - (c > 0));
-        } else {
-          const u64 c = ctr.get(x) - 1u;
-          if (c) {
-            local += c;
-            if (per_edge) {
-              atomicAdd(&c4s[qq[u]], c);  // edge w-x
-              if (pp[u] != ptop) {
-                if (top) atomicAdd(&c4s[ptop], top);
-                top = 0;
-                ptop = pp[u];
-              }
-              top += c;
+    for (int u = 0; u < U; u++) {
+      if (i + 32 * u >= c1) continue;
+      const int x = xx[u];
+      if (MODE == kCount) {
+        ctr.inc(x);
+      } else if (MODE == kZero) {
+        ctr.zero(x);
+      } else if (MODE == kTake) {
+        const u64 c = ctr.take(x);
+        local += c * (c - (c > 0));
+      } else {
+        const u64 c = ctr.get(x) - 1u;
+        if (c) {
+          local += c;
+          if (per_edge) {
+            atomicAdd(&c4s[qq[u]], c);  // edge w-x
+            if (pp[u] != ptop) {
+              if (top) atomicAdd(&c4s[ptop], top);
+              top = 0;
+              ptop = pp[u];
             }
+            top += c;
           }
         }
       }
     }
-    if (MODE == kUse && per_edge && top) atomicAdd(&c4s[ptop], top);
   }
+  if (MODE == kUse && per_edge && top) atomicAdd(&c4s[ptop], top);
   return local;
 }
 
@@ -928,141 +923,149 @@ k_c4_cluster(View g, const int64_t* __restrict__ WP, const int* __restrict__ fra
   }
 }
 
-// Cooperative rounds for the heavy frames.  All CTAs are co-resident
-// (cooperative launch) and walk the same round schedule: a round is up to F
-// frames whose u16 counter slabs stay L2-resident; its items are cut into
-// chunks of CH items spread over the whole grid.
-//   step r:  count(round r) + zero(round r-1)  | barrier |  use(round r) | barrier
-// Two slab sets alternate so zeroing round r-1 overlaps counting round r.
-struct RoundPlan {
+// Heavy frames (more than 24576 wedges, n too large for cluster shared
+// memory) as a dataflow of tasks with no grid barrier.  Frames are grouped in
+// rounds of F frames (one dense u16 counter slab each, ranks [x0, n)); a
+// round's wedge items are cut into chunks.  One task sequence is handed out in
+// order by a global counter:
+//   step t:  C(t) count chunks of round t | U(t-1) use chunks (or S(t-1) slab
+//            scans in global mode) | Z(t-2) zeroing of round t-2's slabs
+// with three slab sets (round r uses set r % 3).  A task waits (spins) only
+// on a segment handed out earlier: U(r), S(r) on C(r); Z(r) on U(r); C(t) on
+// the segment that freed its set (Z(t-3) or S(t-3)).  Every awaited task is
+// therefore already running on a resident CTA, so the kernel needs neither a
+// cooperative launch nor co-residency, and a CTA that finishes early takes
+// the next task instead of idling at a barrier.
+enum FlowType { kFlowCount = 0, kFlowUse = 1, kFlowScan = 2, kFlowZeroSweep = 3, kFlowZeroFill = 4 };
+
+struct FlowSeg {
+  int type, round;
+  int64_t task0, ntasks;  // global task range [task0, task0 + ntasks)
+  int dep;                // segment awaited (-1: none); needs all its tasks done
+};
+
+struct FlowPlan {
   const int* frames;    // heavy frames (rank ids), descending wedges
   const int64_t* cpre;  // [nf+1] chunk prefix
   const int* rf;        // [R+1] round -> first frame index
   const int64_t* rch;   // [R] items per chunk of each round
-  const int* rzs;       // [R] 1: zero the round's counters by a sweep over its wedges
-  const int* rscan;     // [R] 1 (global mode): sums and zeroing by a scan of the slabs
-  int R;                // rounds
-  int F;                // max frames per round (slabs per set)
-  int T;                // independent teams of CTAs (round r belongs to team r % T)
+  const FlowSeg* segs;  // [nseg]
+  int nseg;
+  int F;                // slabs per set
   int64_t slab_words;   // 32-bit words per slab
+  int x0;               // first counter (even): counters cover ranks [x0, n)
+  int64_t pieces;       // uint4 per fill / scan piece
 };
 
-// Barrier among the `members` co-resident CTAs of one team.
-__device__ __forceinline__ void team_barrier(unsigned* bar, unsigned members, unsigned& gen) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned gen0 = gen;
-    const unsigned arrived = atomicAdd(&bar[0], 1u) + 1u;
-    if (arrived == members) {
-      bar[0] = 0u;
-      __threadfence();
-      atomicAdd(&bar[1], 1u);
-    } else {
-      while (*(volatile unsigned*)&bar[1] == gen0) __nanosleep(64);
-    }
-    __threadfence();
+template <int NT, int MODE, int U>
+__device__ __forceinline__ u64 flow_chunk(const View& g, const int64_t* __restrict__ WP, const FlowPlan& P, int r,
+                          int64_t k, unsigned* __restrict__ set, bool per_edge, u64* __restrict__ c4s,
+                          int& s_out) {
+  const int f0 = P.rf[r], f1 = P.rf[r + 1];
+  k += P.cpre[f0];
+  int lo = f0, hi = f1;  // frame of chunk k: last j with cpre[j] <= k
+  while (lo < hi - 1) {
+    int mid = (lo + hi) >> 1;
+    if (P.cpre[mid] <= k) lo = mid; else hi = mid;
   }
-  gen++;
-  __syncthreads();
+  const int j = lo;
+  const int s = P.frames[j];
+  s_out = s;
+  const int64_t b = g.rp[s], o = g.osplit[s];
+  const int64_t fi0 = WP[b], fi1 = WP[o];
+  const int64_t CH = P.rch[r];
+  const int64_t i0 = fi0 + (k - P.cpre[j]) * CH;
+  const int64_t i1 = i0 + CH < fi1 ? i0 + CH : fi1;
+  U16Counter ctr{set + (size_t)(j - f0) * P.slab_words - (P.x0 >> 1)};
+  return wedge_sweep<NT, MODE, U16Counter, U>(g, WP, b, o, i0, i1, ctr, per_edge, c4s);
 }
 
-template <int NT, int MODE>
-__device__ void round_chunks(const View& g, const int64_t* __restrict__ WP, const RoundPlan& P,
-                             int r, unsigned* __restrict__ set, int tb, int ts, bool per_edge,
-                             u64* __restrict__ c4s, u64* __restrict__ c4tot2) {
+template <int NT, int MINB, int U, int UU>
+__global__ void __launch_bounds__(NT, MINB)
+k_c4_flow(View g, const int64_t* __restrict__ WP, FlowPlan P, unsigned* __restrict__ slabs,
+          int per_edge, u64* __restrict__ c4s, u64* __restrict__ c4tot2,
+          unsigned long long* __restrict__ next_task, int* __restrict__ done) {
   typedef cub::BlockReduce<u64, NT> BR;
   __shared__ typename BR::TempStorage tmp;
-  const int f0 = P.rf[r], f1 = P.rf[r + 1];
-  const int64_t k0 = P.cpre[f0], k1 = P.cpre[f1];
-  for (int64_t k = k0 + tb; k < k1; k += ts) {
-    int lo = f0, hi = f1;  // frame of chunk k: last j with cpre[j] <= k
+  __shared__ long long s_task;
+  const int64_t total = P.segs[P.nseg - 1].task0 + P.segs[P.nseg - 1].ntasks;
+  const size_t set_words = (size_t)P.F * P.slab_words;
+  if (threadIdx.x == 0) s_task = (long long)atomicAdd(next_task, 1ull);
+  while (true) {
+    __syncthreads();
+    const int64_t task = s_task;
+    if (task >= total) break;
+    // the next task is claimed now (its latency overlaps this one); it can
+    // only wait on tasks handed out before it, so holding it is safe
+    long long nxt = 0;
+    if (threadIdx.x == 0) nxt = (long long)atomicAdd(next_task, 1ull);
+    int lo = 0, hi = P.nseg;  // segment of the task: last with task0 <= task
     while (lo < hi - 1) {
       int mid = (lo + hi) >> 1;
-      if (P.cpre[mid] <= k) lo = mid; else hi = mid;
+      if (P.segs[mid].task0 <= task) lo = mid; else hi = mid;
     }
-    const int j = lo;
-    const int s = P.frames[j];
-    const int64_t b = g.rp[s], o = g.osplit[s];
-    const int64_t fi0 = WP[b], fi1 = WP[o];
-    const int64_t CH = P.rch[r];
-    const int64_t i0 = fi0 + (k - P.cpre[j]) * CH;
-    const int64_t i1 = i0 + CH < fi1 ? i0 + CH : fi1;
-    U16Counter ctr{set + (size_t)(j - f0) * P.slab_words};
-    const u64 local = wedge_sweep<NT, MODE>(g, WP, b, o, i0, i1, ctr, per_edge, c4s);
-    if (MODE == kUse) {
+    const FlowSeg sg = P.segs[lo];
+    if (threadIdx.x == 0 && sg.dep >= 0) {
+      const int need = (int)P.segs[sg.dep].ntasks;
+      while (*(volatile int*)&done[sg.dep] < need) __nanosleep(128);
+      __threadfence();  // acquire: later loads see the awaited tasks' writes
+    }
+    __syncthreads();
+    const int64_t k = task - sg.task0;
+    const int r = sg.round;
+    unsigned* set = slabs + (size_t)(r % 3) * set_words;
+    if (sg.type == kFlowCount) {
+      int s;
+      flow_chunk<NT, kCount, U>(g, WP, P, r, k, set, false, c4s, s);
+    } else if (sg.type == kFlowUse) {
+      int s;
+      const u64 local = flow_chunk<NT, kUse, UU>(g, WP, P, r, k, set, per_edge != 0, c4s, s);
       const u64 sum = BR(tmp).Sum(local);
       if (threadIdx.x == 0 && sum) atomic_add_u128(c4tot2 + 2 * graph_of(g, s), sum);
-      __syncthreads();
+    } else if (sg.type == kFlowZeroSweep) {
+      int s;
+      flow_chunk<NT, kZero, U>(g, WP, P, r, k, set, false, c4s, s);
+    } else {
+      // piece k of the round's used slabs: fill with zeros, or (global mode)
+      // sum 2*C(c,2) of its counters and zero them
+      const int64_t per_slab = (P.slab_words / 4 + P.pieces - 1) / P.pieces;
+      const int64_t fj = k / per_slab, pc = k - fj * per_slab;
+      uint4* z = (uint4*)(set + (size_t)fj * P.slab_words);
+      const int64_t e0 = pc * P.pieces;
+      const int64_t e1 = e0 + P.pieces < P.slab_words / 4 ? e0 + P.pieces : P.slab_words / 4;
+      const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
+      if (sg.type == kFlowZeroFill) {
+        for (int64_t i = e0 + threadIdx.x; i < e1; i += NT) z[i] = zero4;
+      } else {
+        u64 local = 0;
+        for (int64_t i = e0 + threadIdx.x; i < e1; i += NT) {
+          const uint4 w4 = z[i];
+          const unsigned wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+          for (int t = 0; t < 4; t++) {
+            const u64 c0 = wv[t] & 0xffffu, c1 = wv[t] >> 16;
+            local += c0 * (c0 - (c0 > 0)) + c1 * (c1 - (c1 > 0));
+          }
+          if (wv[0] | wv[1] | wv[2] | wv[3]) z[i] = zero4;
+        }
+        const u64 sum = BR(tmp).Sum(local);
+        if (threadIdx.x == 0 && sum)
+          atomic_add_u128(c4tot2 + 2 * graph_of(g, P.frames[P.rf[r] + fj]), sum);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();  // release: this task's writes before its completion
+      atomicAdd(&done[lo], 1);
+      s_task = nxt;
     }
   }
 }
 
-template <int NT>
-__global__ void __launch_bounds__(NT)
-k_c4_rounds(View g, const int64_t* __restrict__ WP, RoundPlan P, unsigned* __restrict__ slabs,
-            int per_edge, u64* __restrict__ c4s, u64* __restrict__ c4tot2,
-            unsigned* __restrict__ bar) {
-  // teams run their rounds independently: while one team waits at its
-  // barrier, the other teams' CTAs on the same SMs keep working
-  const int team = blockIdx.x % P.T, tb = blockIdx.x / P.T;
-  const int ts = (gridDim.x - team + P.T - 1) / P.T;
-  unsigned* tbar = bar + 2 * team;
-  unsigned* sets = slabs + (size_t)team * 2 * P.F * P.slab_words;
-  unsigned gen = 0;
-  int prev = -1, it = 0;
-  bool prev_scan = false;
-  typedef cub::BlockReduce<u64, NT> BR;
-  __shared__ typename BR::TempStorage tmp;
-  for (int r = team; ; r += P.T, it++) {
-    unsigned* set = sets + (size_t)(it & 1) * P.F * P.slab_words;
-    if (r < P.R) round_chunks<NT, kCount>(g, WP, P, r, set, tb, ts, false, c4s, c4tot2);
-    if (prev >= 0) {
-      unsigned* pset = sets + (size_t)((it - 1) & 1) * P.F * P.slab_words;
-      const int f0 = P.rf[prev], used = P.rf[prev + 1] - f0;
-      if (prev_scan) {
-        // global mode, wedge-heavy round: 2*C(c,2) straight from the counter
-        // slabs (a sequential scan, far shorter than the wedge list), zeroing
-        // them on the way
-        for (int fj = 0; fj < used; fj++) {
-          uint4* z = (uint4*)(pset + (size_t)fj * P.slab_words);
-          u64 local = 0;
-          for (int64_t i = tb * (int64_t)NT + threadIdx.x; i < P.slab_words / 4;
-               i += (int64_t)ts * NT) {
-            const uint4 w4 = z[i];
-            const unsigned wv[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-            for (int t = 0; t < 4; t++) {
-              const u64 c0 = wv[t] & 0xffffu, c1 = wv[t] >> 16;
-              local += c0 * (c0 - (c0 > 0)) + c1 * (c1 - (c1 > 0));
-            }
-            if (wv[0] | wv[1] | wv[2] | wv[3]) z[i] = make_uint4(0u, 0u, 0u, 0u);
-          }
-          const u64 sum = BR(tmp).Sum(local);
-          if (threadIdx.x == 0 && sum)
-            atomic_add_u128(c4tot2 + 2 * graph_of(g, P.frames[f0 + fj]), sum);
-          __syncthreads();
-        }
-      } else if (P.rzs[prev]) {
-        // zero by a sweep over the round's wedges when they touch few counters
-        round_chunks<NT, kZero>(g, WP, P, prev, pset, tb, ts, false, c4s, c4tot2);
-      } else {
-        uint4* z = (uint4*)pset;
-        const int64_t nz = (int64_t)used * P.slab_words / 4;
-        const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
-        for (int64_t i = tb * (int64_t)NT + threadIdx.x; i < nz; i += (int64_t)ts * NT)
-          z[i] = zero4;
-      }
-    }
-    if (r >= P.R) break;
-    team_barrier(tbar, ts, gen);
-    prev_scan = !per_edge && P.rscan[r];
-    if (!prev_scan) {
-      round_chunks<NT, kUse>(g, WP, P, r, set, tb, ts, per_edge != 0, c4s, c4tot2);
-      team_barrier(tbar, ts, gen);
-    }
-    prev = r;
-  }
+// number of isolated vertices: they hold the lowest ranks (degree 0)
+__global__ void k_isolated(View g, int* __restrict__ out) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r < g.n && g.deg[r] == 0 && (r + 1 == g.n || g.deg[r + 1] > 0)) *out = (int)(r + 1);
 }
 
 // ------------------------------------------------------------------------
@@ -1395,7 +1398,7 @@ void set_smem(K kernel, size_t bytes) {
 // against the oracle on small graphs.  Results never depend on the path.
 struct ForcePaths {
   bool tri_gmem = false, tri_small = false, tri_blocks = false, c4_smem = false,
-       c4_coop = false, c4_hub32 = false;
+       c4_coop = false, c4_hub32 = false, c4_flow = false;
 };
 
 ForcePaths read_force() {
@@ -1409,6 +1412,9 @@ ForcePaths read_force() {
   f.c4_smem = v.find("c4_smem") != std::string::npos;
   f.c4_coop = v.find("c4_coop") != std::string::npos;
   f.c4_hub32 = v.find("c4_hub32") != std::string::npos;
+  // heavy-frame schedulers on any graph size: cluster path off, two frames
+  // per round (many rounds, every slab set reused)
+  f.c4_flow = v.find("c4_flow") != std::string::npos;
   return f;
 }
 
@@ -1674,7 +1680,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   stat("wedges", total_w);
   stat("tri_items", tot_items);
   int64_t t0 = 256, t1 = 4096, t2 = 24576;
-  if (force.c4_coop || force.c4_hub32) t0 = t1 = t2 = 0;
+  if (force.c4_coop || force.c4_hub32 || force.c4_flow) t0 = t1 = t2 = 0;
   if (force.c4_smem) t0 = t1 = 0;  // every frame <= t2 through the u16 hash
   const auto wr = wk.ranges({{1, t0}, {t0 + 1, t1}, {t1 + 1, t2}, {t2 + 1, INT64_MAX}});
   const auto rs0 = wr[0], rs1 = wr[1], rs2 = wr[2], rh = wr[3];
@@ -1715,7 +1721,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     // clusters measured slower than the L2 rounds: hot counters serialise
     // on one SM's shared memory and only 7 16-CTA clusters are resident)
     int csize = 0, per = 0;
-    if (env_int("GD_C4_CLUSTER", 1)) {
+    if (env_int("GD_C4_CLUSTER", 1) && !force.c4_flow) {
       const int64_t max_per = 98304;  // u16 counters per CTA (192 KB)
       const int cmax = (int)env_int("GD_C4_CLUSTER_MAX", 4);
       for (int c = 1; c <= cmax; c *= 2) {
@@ -1766,66 +1772,102 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     } else if (!f16.empty()) {
       constexpr int NT = 512;
       int per_sm = 0;
-      GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_c4_rounds<NT>, NT, 0));
-      if (per_sm < 1) throw Error(GD_ECUDA, "c4 rounds kernel cannot be resident");
+      // 4 CTAs/SM (32 registers) and 2 items per lane in flight: measured
+      // 72.6 ms vs 87.6 (3 CTAs, 1 item) on config 3; the use sweep's
+      // dependent counter reads are latency-bound
+      auto fk = k_c4_flow<NT, 4, 2, 2>;
+      const int fnt = NT;
+      GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fk, fnt, 0));
+      if (per_sm < 1) throw Error(GD_ECUDA, "c4 flow kernel cannot be resident");
       const int grid = per_sm * num_sms();
-      const int64_t slab_words = (((n + 1) / 2) + 31) & ~int64_t(31);  // multiple of 4
-      const int T = (int)std::max<int64_t>(1, std::min<int64_t>(grid, env_int("GD_C4_TEAMS", 4)));
-      const int64_t l2_budget = env_int("GD_C4_L2_MB", 256) << 20;  // all teams, one set each
-      const int F = (int)std::max<int64_t>(
-          1, std::min<int64_t>(256, l2_budget / (T * slab_words * 4)));
-      // rounds of F frames; each round's chunk size gives >= 2 chunks per CTA
+      // counters cover ranks [x0, n): isolated vertices (the lowest ranks)
+      // never end a wedge
+      int x0 = 0;
+      {
+        int* d0 = ws_get<int>(g, "x0", 1, s);
+        GD_CUDA(cudaMemsetAsync(d0, 0, 4, s));
+        k_isolated<<<grid_cap(n, 256), 256, 0, s>>>(v, d0);
+        GD_LAUNCH_CHECK("isolated");
+        GD_CUDA(cudaMemcpyAsync(&x0, d0, 4, cudaMemcpyDeviceToHost, s));
+        GD_CUDA(cudaStreamSynchronize(s));
+        x0 &= ~1;
+      }
+      const int64_t slab_words = ((((int64_t)n - x0) + 1) / 2 + 31) & ~int64_t(31);
+      const int64_t l2_budget = env_int("GD_C4_FLOW_MB", 320) << 20;  // three slab sets
+      const int F = force.c4_flow ? 2 : (int)std::max<int64_t>(
+          1, std::min<int64_t>(256, l2_budget / (3 * slab_words * 4)));
+      const int64_t pieces = force.c4_flow ? 8 : 16384;  // uint4 per fill / scan task
+      const int64_t per_slab = (slab_words / 4 + pieces - 1) / pieces;
+      const int64_t min_ch = force.c4_flow ? 1 : env_int("GD_C4_MIN_CHUNK", 16384);
+      const int64_t max_ch = std::max(min_ch, env_int("GD_C4_MAX_CHUNK", 65536));
       std::vector<int> rf, rzs, rscan;
       std::vector<int64_t> rch, cpre(f16.size() + 1, 0);
       for (size_t j0 = 0; j0 < f16.size(); j0 += F) {
         const size_t j1 = std::min(f16.size(), j0 + (size_t)F);
         int64_t wr = 0;
         for (size_t j = j0; j < j1; j++) wr += w16[j];
-        // a zero sweep rewrites <= wr scattered 2-byte counters (~32 B of
-        // traffic each), a memset streams (j1-j0) slabs
         rzs.push_back(wr * 32 < (int64_t)(j1 - j0) * slab_words * 4 ? 1 : 0);
-        // a slab scan reads 4 B per counter pair sequentially, the use sweep
-        // ~32 B per wedge scattered
-        rscan.push_back(wr * 32 > (int64_t)(j1 - j0) * slab_words * 4 * 2 ? 1 : 0);
-        int64_t ch = wr / (2 * (int64_t)(grid / T));
-        ch = std::max<int64_t>(1024, std::min<int64_t>(65536, (ch + 511) & ~int64_t(511)));
+        rscan.push_back(!per_edge && wr * 32 > (int64_t)(j1 - j0) * slab_words * 4 * 2 ? 1 : 0);
+        int64_t ch = wr / (2 * (int64_t)grid);
+        ch = std::max<int64_t>(min_ch, std::min<int64_t>(max_ch, (ch + 511) & ~int64_t(511)));
+        if (force.c4_flow) ch = 64;  // many small tasks
         rf.push_back((int)j0);
         rch.push_back(ch);
         for (size_t j = j0; j < j1; j++) cpre[j + 1] = cpre[j] + (w16[j] + ch - 1) / ch;
       }
       rf.push_back((int)f16.size());
-      DBuf<int> dfr, drf, drzs, drscan;
+      const int R = (int)rf.size() - 1;
+      std::vector<FlowSeg> segs;
+      std::vector<int> freed(R, -1), cseg(R, -1), useg(R, -1);
+      int64_t task0 = 0;
+      auto add = [&](int type, int r, int64_t nt, int dep) {
+        segs.push_back(FlowSeg{type, r, task0, nt, dep});
+        task0 += nt;
+        return (int)segs.size() - 1;
+      };
+      for (int t = 0; t <= R + 1; t++) {
+        if (t < R)
+          cseg[t] = add(kFlowCount, t, cpre[rf[t + 1]] - cpre[rf[t]], t >= 3 ? freed[t - 3] : -1);
+        const int r1 = t - 1;
+        if (r1 >= 0 && r1 < R) {
+          const int64_t used = rf[r1 + 1] - rf[r1];
+          if (rscan[r1]) freed[r1] = add(kFlowScan, r1, used * per_slab, cseg[r1]);
+          else useg[r1] = add(kFlowUse, r1, cpre[rf[r1 + 1]] - cpre[rf[r1]], cseg[r1]);
+        }
+        const int r2 = t - 2;
+        if (r2 >= 0 && r2 < R && !rscan[r2] && r2 + 3 < R) {
+          const int64_t used = rf[r2 + 1] - rf[r2];
+          freed[r2] = rzs[r2] ? add(kFlowZeroSweep, r2, cpre[rf[r2 + 1]] - cpre[rf[r2]], useg[r2])
+                              : add(kFlowZeroFill, r2, used * per_slab, useg[r2]);
+        }
+      }
+      DBuf<int> dfr, drf, done;
       DBuf<int64_t> dcp, drch;
-      DBuf<unsigned> slabs, bar;
+      DBuf<FlowSeg> dseg;
+      DBuf<unsigned long long> ntask;
       dfr.alloc(f16.size(), s);
       drf.alloc(rf.size(), s);
-      drzs.alloc(rzs.size(), s);
-      GD_CUDA(cudaMemcpyAsync(drzs.p, rzs.data(), rzs.size() * 4, cudaMemcpyHostToDevice, s));
-      drscan.alloc(rscan.size(), s);
-      GD_CUDA(cudaMemcpyAsync(drscan.p, rscan.data(), rscan.size() * 4, cudaMemcpyHostToDevice,
-                              s));
       dcp.alloc(cpre.size(), s);
       drch.alloc(rch.size(), s);
-      slabs.alloc((size_t)T * 2 * F * slab_words, s);
-      slabs.zero();
-      bar.alloc(2 * T, s);
-      bar.zero();
+      dseg.alloc(segs.size(), s);
+      done.alloc(segs.size(), s);
+      done.zero();
+      ntask.alloc(1, s);
+      ntask.zero();
       GD_CUDA(cudaMemcpyAsync(dfr.p, f16.data(), f16.size() * 4, cudaMemcpyHostToDevice, s));
       GD_CUDA(cudaMemcpyAsync(drf.p, rf.data(), rf.size() * 4, cudaMemcpyHostToDevice, s));
       GD_CUDA(cudaMemcpyAsync(dcp.p, cpre.data(), cpre.size() * 8, cudaMemcpyHostToDevice, s));
       GD_CUDA(cudaMemcpyAsync(drch.p, rch.data(), rch.size() * 8, cudaMemcpyHostToDevice, s));
-      RoundPlan P{dfr.p, dcp.p, drf.p, drch.p, drzs.p, drscan.p, (int)rf.size() - 1, F, T,
-                  slab_words};
-      nrounds += P.R;
-      unsigned* slabs_p = slabs.p;
-      unsigned* bar_p = bar.p;
-      const int64_t* WP_p = WP.p;
-      u64* c4t_p = c4tot2.p;
-      void* args[] = {(void*)&v, (void*)&WP_p, (void*)&P, (void*)&slabs_p, (void*)&pe,
-                      (void*)&c4s_p, (void*)&c4t_p, (void*)&bar_p};
-      GD_CUDA(cudaLaunchCooperativeKernel((void*)k_c4_rounds<NT>, dim3(grid), dim3(NT), args, 0,
-                                          s));
-      GD_LAUNCH_CHECK("c4_rounds");
+      GD_CUDA(cudaMemcpyAsync(dseg.p, segs.data(), segs.size() * sizeof(FlowSeg),
+                              cudaMemcpyHostToDevice, s));
+      const size_t slab_total = (size_t)3 * F * slab_words;
+      unsigned* slabs = ws_get<unsigned>(g, "c4_slabs", slab_total, s);
+      GD_CUDA(cudaMemsetAsync(slabs, 0, slab_total * 4, s));
+      FlowPlan P{dfr.p, dcp.p, drf.p, drch.p, dseg.p, (int)segs.size(), F, slab_words, x0,
+                 pieces};
+      nrounds += R;
+      fk<<<grid, fnt, 0, s>>>(v, WP.p, P, slabs, pe, c4s_p, c4tot2.p, ntask.p, done.p);
+      GD_LAUNCH_CHECK("c4_flow");
     }
     timer.mark("c4_coop");
     if (!f32.empty()) {

@@ -61,7 +61,7 @@ def test_degenerate_graphs():
 
 
 FORCED = ["tri_gmem", "tri_small", "tri_blocks", "c4_coop", "c4_hub32", "c4_smem",
-          "tri_gmem,c4_coop", "tri_small,c4_hub32"]
+          "c4_flow", "tri_gmem,c4_coop", "tri_small,c4_hub32"]
 
 
 def _dense_cases():
