@@ -1537,6 +1537,13 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     struct B { int64_t lo, hi; int nt; bool gmem; };
     std::vector<B> bins = {{1025, INT64_MAX, 512, true}, {513, 1024, 512, false},
                            {129, 512, 256, false}, {33, 128, 128, false}, {2, 32, 32, false}};
+    if (env_int("GD_TRI_SPLIT", 1) == 1)
+      bins = {{1025, INT64_MAX, 512, true}, {513, 1024, 512, false}, {257, 512, 256, false},
+              {129, 256, 256, false}, {65, 128, 128, false}, {33, 64, 128, false},
+              {2, 32, 32, false}};
+    if (env_int("GD_TRI_SPLIT", 1) == 2)
+      bins = {{1025, INT64_MAX, 512, true}, {513, 1024, 512, false}, {257, 512, 256, false},
+              {129, 256, 128, false}, {33, 128, 128, false}, {2, 32, 32, false}};
     int64_t stage_max = 1 << 20;
     if (force.tri_gmem) bins = {{2, INT64_MAX, 512, true}};
     if (force.tri_small) bins = {{2, INT64_MAX, 32, false}}, stage_max = 16;
@@ -1679,11 +1686,12 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   }
   stat("wedges", total_w);
   stat("tri_items", tot_items);
-  int64_t t0 = 256, t1 = 4096, t2 = 24576;
-  if (force.c4_coop || force.c4_hub32 || force.c4_flow) t0 = t1 = t2 = 0;
-  if (force.c4_smem) t0 = t1 = 0;  // every frame <= t2 through the u16 hash
-  const auto wr = wk.ranges({{1, t0}, {t0 + 1, t1}, {t1 + 1, t2}, {t2 + 1, INT64_MAX}});
-  const auto rs0 = wr[0], rs1 = wr[1], rs2 = wr[2], rh = wr[3];
+  int64_t t0 = 256, ta = 1024, t1 = 4096, tb = 12288, t2 = 24576;
+  if (force.c4_coop || force.c4_hub32 || force.c4_flow) t0 = ta = t1 = tb = t2 = 0;
+  if (force.c4_smem) t0 = ta = t1 = 0;  // every frame <= t2 through the u16 hashes
+  const auto wr = wk.ranges({{1, t0}, {t0 + 1, ta}, {ta + 1, t1}, {t1 + 1, tb}, {tb + 1, t2},
+                             {t2 + 1, INT64_MAX}});
+  const auto rs0 = wr[0], rsa = wr[1], rs1 = wr[2], rsb = wr[3], rs2 = wr[4], rh = wr[5];
   const int pe = per_edge ? 1 : 0;
   u64* c4s_p = per_edge ? c4s.p : nullptr;
   const int64_t nh = rh.second - rh.first;
@@ -1930,8 +1938,12 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       GD_LAUNCH_CHECK("c4_frames_smem");
     }
   };
+  // hash capacity grows with the bin's largest frame: finer bins keep more
+  // CTAs resident per SM (u16 counts above 4096 wedges)
   smem_bin(rs2, k_c4_frames_smem<512, true>, 512, true, 1);
+  smem_bin(rsb, k_c4_frames_smem<512, true>, 512, true, 2);
   smem_bin(rs1, k_c4_frames_smem<256, false>, 256, false, 3);
+  smem_bin(rsa, k_c4_frames_smem<128, false>, 128, false, 12);
   smem_bin(rs0, k_c4_frames_smem<64, false>, 64, false, 32);
   timer.mark("c4_smem");
   if (sh.real() && per_edge) {  // per-slot triangle sums and 4-cycle counts of all shards
@@ -1944,7 +1956,8 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   stat("c4_coop_frames", nh - n32);
   stat("c4_rounds", nrounds);
   stat("c4_u32_hub_frames", n32);
-  stat("c4_smem_frames", (rs0.second - rs0.first) + (rs1.second - rs1.first) +
+  stat("c4_smem_frames", (rs0.second - rs0.first) + (rsa.second - rsa.first) +
+                             (rs1.second - rs1.first) + (rsb.second - rsb.first) +
                              (rs2.second - rs2.first));
 
   // ---- finalize -----------------------------------------------------------
