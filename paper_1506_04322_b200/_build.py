@@ -30,14 +30,18 @@ def _needs(obj: Path, deps) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
-    BUILD.mkdir(exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines=(), lib: Path = LIB,
+          objdir: Path = BUILD) -> Path:
+    """Compile the library; `defines` (-DNAME=V) build an experiment variant
+    into `lib` / `objdir` (tools/build_variant.py)."""
+    LIB, BUILD = lib, objdir
+    BUILD.mkdir(parents=True, exist_ok=True)
     headers = list(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "gd_api.h"]
     jobs = []
     for src in SOURCES:
         obj = BUILD / (Path(src).stem + ".o")
         if force or _needs(obj, [CSRC / src] + headers):
-            jobs.append([NVCC, *FLAGS, "-Xptxas", "-v" if verbose else "-O3",
+            jobs.append([NVCC, *FLAGS, *defines, "-Xptxas", "-v" if verbose else "-O3",
                          "-c", str(CSRC / src), "-o", str(obj)])
 
     def run(cmd):

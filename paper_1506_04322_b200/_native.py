@@ -78,7 +78,9 @@ def load_library(path: Path | None = None):
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        # GD_LIBRARY: an alternative build of the same library (schedule
+        # experiments, tools/build_variant.py); never a different backend
+        p = Path(path) if path else Path(os.environ.get("GD_LIBRARY", LIB_PATH))
         if not p.exists():
             raise DeviceError(f"{p} is missing: build it with __graft_entry__.build() "
                               "(there is no CPU fallback)")
