@@ -1563,11 +1563,14 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     std::vector<B> bins = {{1025, INT64_MAX, 512, true}, {513, 1024, 512, false},
                            {129, 512, 256, false}, {33, 128, 128, false}, {2, 32, 32, false}};
     if (env_int("GD_TRI_SPLIT", 1) == 1)
-      bins = {{1025, INT64_MAX, 512, true}, {513, 1024, 512, false}, {257, 512, 256, false},
-              {129, 256, 256, false}, {65, 128, 128, false}, {33, 64, 128, false},
+      bins = {{1025, INT64_MAX, (int)env_int("GD_TRI_GM_NT", 1024), true},
+              {513, 1024, (int)env_int("GD_TRI_B1024_NT", 1024), false},
+              {257, 512, (int)env_int("GD_TRI_B512_NT", 512), false},
+              {129, 256, (int)env_int("GD_TRI_B256_NT", 256), false}, {65, 128, 128, false}, {33, 64, 128, false},
               {2, 32, 32, false}};
     if (env_int("GD_TRI_SPLIT", 1) == 2)
-      bins = {{1025, INT64_MAX, 512, true}, {513, 1024, 512, false}, {257, 512, 256, false},
+      bins = {{1025, INT64_MAX, 512, true}, {513, 1024, 512, false},
+              {257, 512, (int)env_int("GD_TRI_B512_NT", 256), false},
               {129, 256, 128, false}, {33, 128, 128, false}, {2, 32, 32, false}};
     int64_t stage_max = 1 << 20;
     if (force.tri_gmem) bins = {{2, INT64_MAX, 512, true}};
@@ -1618,6 +1621,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     }                                                                                        \
   }
       switch (bn.nt) {
+        case 1024: GD_OCC(1024) break;
         case 512: GD_OCC(512) break;
         case 256: GD_OCC(256) break;
         case 128: GD_OCC(128) break;
@@ -1674,6 +1678,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     GD_LAUNCH_CHECK("trisum_frames");                                                        \
   }
       switch (bn.nt) {
+        case 1024: GD_TRI_LAUNCH(1024) break;
         case 512: GD_TRI_LAUNCH(512) break;
         case 256: GD_TRI_LAUNCH(256) break;
         case 128: GD_TRI_LAUNCH(128) break;
@@ -1831,7 +1836,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
           1, std::min<int64_t>(256, l2_budget / (3 * slab_words * 4)));
       const int64_t pieces = force.c4_flow ? 8 : 16384;  // uint4 per fill / scan task
       const int64_t per_slab = (slab_words / 4 + pieces - 1) / pieces;
-      const int64_t min_ch = force.c4_flow ? 1 : env_int("GD_C4_MIN_CHUNK", 16384);
+      const int64_t min_ch = force.c4_flow ? 1 : env_int("GD_C4_MIN_CHUNK", 8192);
       const int64_t max_ch = std::max(min_ch, env_int("GD_C4_MAX_CHUNK", 65536));
       std::vector<int> rf, rzs, rscan;
       std::vector<int64_t> rch, cpre(f16.size() + 1, 0);
@@ -1965,8 +1970,14 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   };
   // hash capacity grows with the bin's largest frame: finer bins keep more
   // CTAs resident per SM (u16 counts above 4096 wedges)
-  smem_bin(rs2, k_c4_frames_smem<512, true>, 512, true, 1);
-  smem_bin(rsb, k_c4_frames_smem<512, true>, 512, true, 2);
+  if (env_int("GD_C4_TOP_NT", 1024) == 1024)
+    smem_bin(rs2, k_c4_frames_smem<1024, true>, 1024, true, 1);
+  else
+    smem_bin(rs2, k_c4_frames_smem<512, true>, 512, true, 1);
+  if (env_int("GD_C4_MID_NT", 1024) == 1024)
+    smem_bin(rsb, k_c4_frames_smem<1024, true>, 1024, true, 2);
+  else
+    smem_bin(rsb, k_c4_frames_smem<512, true>, 512, true, 2);
   smem_bin(rs1, k_c4_frames_smem<256, false>, 256, false, 3);
   smem_bin(rsa, k_c4_frames_smem<128, false>, 128, false, 12);
   smem_bin(rs0, k_c4_frames_smem<64, false>, 64, false, 32);
