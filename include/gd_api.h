@@ -186,6 +186,12 @@ GD_API void  gd_host_free(void* p);
 /* Write a buffer larger than L2 on the library stream (timing hygiene). */
 GD_API int gd_flush_l2(void);
 
+/* Release the calling thread's cached census workspace (slot accumulators,
+ * hit buffer, counter slabs).  It is kept between calls so that censuses of
+ * fresh graphs of similar size do not re-allocate; no reference counterpart
+ * (the reference allocates per call, census.py:190-303). */
+GD_API int gd_trim_workspace(void);
+
 #ifdef __cplusplus
 }
 #endif

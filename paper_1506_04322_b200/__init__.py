@@ -11,7 +11,7 @@ from .analytics import FeatureMatrix, GfdVector, feature_matrix, gfd
 from .census import (RAW_MICRO_FIELDS, CensusSums, census_batch, close_quads,
                      close_triads, frequencies_from_micro, frequencies_from_sums,
                      graphlet_census, last_stats, last_timings, micro_census_table,
-                     micro_table)
+                     micro_table, trim_workspace)
 from .classes import (ALL_CLASSES, CLASS_BY_ID, CLASS_IDS, GraphletClass,
                       classes_for, complement_class)
 from .errors import (ClassificationError, ConsistencyError, DeviceError,
@@ -31,7 +31,7 @@ __all__ = [
     "FeatureMatrix", "GfdVector", "feature_matrix", "gfd",
     "RAW_MICRO_FIELDS", "CensusSums", "census_batch", "close_quads", "close_triads",
     "frequencies_from_micro", "frequencies_from_sums", "graphlet_census", "last_stats",
-    "last_timings", "micro_census_table", "micro_table",
+    "last_timings", "micro_census_table", "micro_table", "trim_workspace",
     "ALL_CLASSES", "CLASS_BY_ID", "CLASS_IDS", "GraphletClass", "classes_for",
     "complement_class",
     "ClassificationError", "ConsistencyError", "DeviceError", "EdgeListParseError",

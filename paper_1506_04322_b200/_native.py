@@ -69,6 +69,7 @@ SIGNATURES = (
     ("gd_host_alloc", _vp, [ctypes.c_int64]),
     ("gd_host_free", None, [_vp]),
     ("gd_flush_l2", ctypes.c_int, []),
+    ("gd_trim_workspace", ctypes.c_int, []),
 )
 
 

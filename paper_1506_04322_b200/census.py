@@ -258,6 +258,12 @@ def last_timings(g) -> dict[str, float]:
     return {labels[i]: float(ms[i]) for i in range(k)}
 
 
+def trim_workspace() -> None:
+    """Release this thread's cached device workspace of the census kernels
+    (kept between calls so censuses of fresh graphs do not re-allocate)."""
+    N.check(N.lib().gd_trim_workspace())
+
+
 def last_stats(g) -> dict[str, int]:
     vals = (ctypes.c_int64 * 32)()
     names = ctypes.c_char_p()

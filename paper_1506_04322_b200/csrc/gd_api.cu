@@ -95,6 +95,11 @@ static void init_pool_once() {
   });
 }
 
+std::map<std::string, WsBuf>& thread_workspace() {
+  static thread_local std::map<std::string, WsBuf> w;
+  return w;
+}
+
 static cudaStream_t thread_stream() {
   static thread_local cudaStream_t s = nullptr;
   if (!s) GD_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -550,6 +555,15 @@ int gd_flush_l2(void) {
     if (!buf) GD_CUDA(cudaMalloc(&buf, bytes));
     GD_CUDA(cudaMemsetAsync(buf, (int)(rand() & 0xff), bytes, s));
     GD_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int gd_trim_workspace(void) {
+  return guarded([&] {
+    cudaStream_t s = thread_stream();
+    GD_CUDA(cudaStreamSynchronize(s));
+    GD_CUDA(cudaDeviceSynchronize());
+    thread_workspace().clear();
   });
 }
 

@@ -122,18 +122,42 @@ struct DevGraph {
   DBuf<int64_t> eoff;   // [G+1] canonical edge offsets per graph
   DBuf<int64_t> gn;     // [G] vertex count per graph
   std::vector<int64_t> h_eoff, h_gn;
-  // census workspace: large scratch buffers kept across calls on this graph
-  // (same sizes every call, so repeated censuses never re-allocate)
-  std::map<std::string, DBuf<char>> ws;
   uint64_t hit_cap = 0;      // entries of the persisted hit-list buffer
   bool hit_cap_known = false;
 };
 
+// Census workspace: large scratch buffers (slot accumulators, item prefixes,
+// hit buffer, counter slabs) cached per host thread and reused by every
+// census of every graph on that thread, so a fresh graph of the same size
+// never re-allocates.  Calls are synchronous, so one thread's buffers are
+// idle between calls.  Grown with stream-ordered free + alloc on the calling
+// census stream; released by gd_trim_workspace() or at thread exit.
+struct WsBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  WsBuf() = default;
+  WsBuf(const WsBuf&) = delete;
+  WsBuf& operator=(const WsBuf&) = delete;
+  ~WsBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+std::map<std::string, WsBuf>& thread_workspace();
+
 template <typename T>
-T* ws_get(DevGraph& g, const char* name, size_t count, cudaStream_t s) {
-  DBuf<char>& b = g.ws[name];
+T* ws_get(DevGraph&, const char* name, size_t count, cudaStream_t s) {
+  WsBuf& b = thread_workspace()[name];
   const size_t bytes = count * sizeof(T);
-  if (b.n < bytes) b.alloc(bytes, s);
+  if (b.bytes < bytes) {
+    if (b.p) GD_CUDA(cudaFreeAsync(b.p, s));
+    b.p = nullptr;
+    b.bytes = 0;
+    GD_CUDA(cudaMallocAsync(&b.p, bytes, s));
+    b.bytes = bytes;
+  }
   return (T*)b.p;
 }
 

@@ -796,7 +796,9 @@ __device__ __forceinline__ u64 wedge_sweep(const View& g, const int64_t* __restr
         if (c) {
           local += c;
           if (per_edge) {
+#ifndef GD_EXP_NO_C4S  // timing experiment only (tools/build_variant.py)
             atomicAdd(&c4s[qq[u]], c);  // edge w-x
+#endif
             if (pp[u] != ptop) {
               if (top) atomicAdd(&c4s[ptop], top);
               top = 0;
