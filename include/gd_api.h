@@ -183,6 +183,36 @@ GD_API void  gd_device_free(void* p);
 GD_API void* gd_host_alloc(int64_t bytes);
 GD_API void  gd_host_free(void* p);
 
+/*
+ * Edge-list text on the device.  Replaces load_edge_list (graph.py:223-285)
+ * for ASCII text: the bytes are copied to the GPU once, lines are tokenised
+ * there and the integer pairs stay in device memory, ready for
+ * gd_graph_create(..., GD_INPUT_DEVICE).  `prefixes` are the comment
+ * prefixes (ParseOptions.comment_prefixes, graph.py:44).  Flags:
+ * GD_PARSE_CR_NEWLINE marks text read from a file in universal-newline mode
+ * (a lone '\r' is a line break there); GD_PARSE_MM_SHIFT shifts the ids of a
+ * MatrixMarket file with a size header to 0-based (graph.py:277-283).
+ * gd_parsed_info fills int64 info[12]:
+ *   [0] pairs  [1] MatrixMarket rows or -1
+ *   [2] error kind: 0 none, 1 "expected at least 2 integer tokens",
+ *       2 "non-integer vertex id", 3 "malformed MatrixMarket size header",
+ *       4 "no data lines" (EdgeListParseError, graph.py:257-271)
+ *   [3] error line (1-based)  [4] byte offset  [5] byte length of that line
+ *   [6] nonzero: input outside the ASCII rules (non-ASCII bytes, a lone '\r'
+ *       under GD_PARSE_CR_NEWLINE, ids beyond int64) -- nothing parsed; the
+ *       caller must decide such input with CPython's rules
+ *   [7] min id  [8] max id  [9] shift applied  [10] lines
+ */
+#define GD_PARSE_CR_NEWLINE 1
+#define GD_PARSE_MM_SHIFT   2
+typedef struct gd_parsed gd_parsed;
+GD_API int gd_parse_edge_list(const char* text, int64_t len, const char* const* prefixes,
+                              int nprefixes, int flags, gd_parsed** out);
+GD_API int gd_parsed_info(const gd_parsed* p, int64_t* info);
+/* Device pointer of the parsed int64 [pairs][2] array (valid until freed). */
+GD_API const int64_t* gd_parsed_pairs(const gd_parsed* p);
+GD_API void gd_parsed_free(gd_parsed* p);
+
 /* Write a buffer larger than L2 on the library stream (timing hygiene). */
 GD_API int gd_flush_l2(void);
 

@@ -12,6 +12,7 @@ from .census import (RAW_MICRO_FIELDS, CensusSums, census_batch, close_quads,
                      close_triads, frequencies_from_micro, frequencies_from_sums,
                      graphlet_census, last_stats, last_timings, micro_census_table,
                      micro_table, trim_workspace)
+from .edgelist import load_edge_list, to_edge_list_text
 from .classes import (ALL_CLASSES, CLASS_BY_ID, CLASS_IDS, GraphletClass,
                       classes_for, complement_class)
 from .errors import (ClassificationError, ConsistencyError, DeviceError,
@@ -38,6 +39,7 @@ __all__ = [
     "GraphletError", "GraphSizeError",
     "GraphletFrequencies",
     "EdgeRef", "Graph", "GraphBatch", "ParseOptions", "order_edges_by_degree",
+    "load_edge_list", "to_edge_list_text",
     "MAX_BATCH_SIZE", "ParallelConfig", "WorkerFailure",
     "MICRO_CSV_HEADER", "EdgeLocalCounts", "MicroCounts", "UnrestrictedCounts", "derive_micro",
     "micro_census", "micro_counts_from_table", "micro_csv", "unrestricted_counts",

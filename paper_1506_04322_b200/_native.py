@@ -21,6 +21,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libgdgpu.so"
 GD_OK, GD_EINVAL, GD_EPARSE, GD_ECAPACITY, GD_ECUDA, GD_ECONSISTENCY = 0, -1, -2, -3, -4, -5
 GD_IDS_REMAP, GD_IDS_DECLARED, GD_IDS_MAX_ID, GD_IDS_SANITIZED = 0, 1, 2, 3
 GD_INPUT_DEVICE, GD_OUTPUT_DEVICE = 1, 2
+GD_PARSE_CR_NEWLINE, GD_PARSE_MM_SHIFT = 1, 2
 NUM_SUMS, NUM_MICRO = 13, 10
 
 _lib = None
@@ -70,6 +71,12 @@ SIGNATURES = (
     ("gd_host_free", None, [_vp]),
     ("gd_flush_l2", ctypes.c_int, []),
     ("gd_trim_workspace", ctypes.c_int, []),
+    ("gd_parse_edge_list", ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64,
+                                          ctypes.POINTER(ctypes.c_char_p), ctypes.c_int,
+                                          ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    ("gd_parsed_info", ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int64)]),
+    ("gd_parsed_pairs", _vp, [_vp]),
+    ("gd_parsed_free", None, [_vp]),
 )
 
 

@@ -7,6 +7,7 @@
 
 #include "gd_build.cuh"
 #include "gd_count.cuh"
+#include "gd_parse.cuh"
 
 struct gd_graph {
   gd::DevGraph g;
@@ -556,6 +557,48 @@ int gd_flush_l2(void) {
     GD_CUDA(cudaMemsetAsync(buf, (int)(rand() & 0xff), bytes, s));
     GD_CUDA(cudaStreamSynchronize(s));
   });
+}
+
+struct gd_parsed {
+  gd::ParseOut out;
+};
+
+int gd_parse_edge_list(const char* text, int64_t len, const char* const* prefixes,
+                       int nprefixes, int flags, gd_parsed** out) {
+  if (!out || (len > 0 && !text) || (nprefixes > 0 && !prefixes)) {
+    t_last_error = "NULL argument";
+    return GD_EINVAL;
+  }
+  *out = nullptr;
+  gd_parsed* p = new gd_parsed();
+  const int rc = guarded([&] {
+    cudaStream_t s = thread_stream();
+    parse_edge_list(text, len, prefixes, nprefixes, (flags & GD_PARSE_CR_NEWLINE) ? 1 : 0,
+                    (flags & GD_PARSE_MM_SHIFT) ? 1 : 0, p->out, s);
+  });
+  if (rc != GD_OK) {
+    delete p;
+    return rc;
+  }
+  *out = p;
+  return GD_OK;
+}
+
+int gd_parsed_info(const gd_parsed* p, int64_t* info) {
+  if (!p || !info) {
+    t_last_error = "NULL argument";
+    return GD_EINVAL;
+  }
+  for (int k = 0; k < 12; k++) info[k] = p->out.info[k];
+  return GD_OK;
+}
+
+const int64_t* gd_parsed_pairs(const gd_parsed* p) { return p ? p->out.pairs.p : nullptr; }
+
+void gd_parsed_free(gd_parsed* p) {
+  if (!p) return;
+  if (p->out.pairs.p) cudaStreamSynchronize(p->out.pairs.s);
+  delete p;
 }
 
 int gd_trim_workspace(void) {

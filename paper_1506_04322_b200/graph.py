@@ -124,6 +124,18 @@ class Graph:
         return Graph(0, None, _handle=_create(arr, 0, N.GD_IDS_REMAP))
 
     @staticmethod
+    def from_file(path, options: ParseOptions | None = None) -> "Graph":
+        """Edge-list file (graph.py:159-162), tokenised on the GPU."""
+        from .edgelist import from_file
+        return from_file(path, options)
+
+    @staticmethod
+    def from_text(text: str, options: ParseOptions | None = None) -> "Graph":
+        """Edge-list text (graph.py:164-166), tokenised on the GPU."""
+        from .edgelist import from_text
+        return from_text(text, options)
+
+    @staticmethod
     def from_reference(g) -> "Graph":
         """Device copy of any graph object with ``n``, ``edges`` (and
         optionally ``orig_ids``), e.g. a reference ``graphlets.Graph``."""

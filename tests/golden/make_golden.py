@@ -257,3 +257,111 @@ def make_micro_roles():
 
 if __name__ == "__main__" and "--roles" in sys.argv:
     make_micro_roles()
+
+
+PARSE_CASES = [
+    # (name, text, opts, modes)  modes: "text" (Graph.from_text), "file"
+    # (Graph.from_file: UTF-8, universal newlines)
+    ("simple", "0 1\n1 2\n2 0\n", {}, ("text", "file")),
+    ("comments", "# header\n% mm comment\n0 1\n  # indented comment\n1 2\n", {}, ("text", "file")),
+    ("commas_third_col", "0,1\n1,2,5.5\n2 3 w=7\n", {}, ("text", "file")),
+    ("whitespace", "\t 3   4 \t\n\n   \n5\t6\n", {}, ("text", "file")),
+    ("crlf", "0 1\r\n1 2\r\n2 0\r\n", {}, ("text", "file")),
+    ("lone_cr", "0 1\r1 2\r2 3\r", {}, ("text", "file")),
+    ("loops_dups_reciprocal", "1 1\n1 2\n2 1\n1 2\n3 1\n", {}, ("text", "file")),
+    ("ids_64bit", "9223372036854775807 5\n-9223372036854775808 5\n", {}, ("text", "file")),
+    ("negative_remap", "-5 3\n3 -5\n-100 7\n", {}, ("text", "file")),
+    ("int_literals", "1_0 2\n+3 -4\n007 8\n0_0 9\n", {}, ("text", "file")),
+    ("no_trailing_newline", "0 1\n1 2", {}, ("text", "file")),
+    ("odd_whitespace", "0\x0b1\n2\x1c3\n4\x0c5\n", {}, ("text", "file")),
+    ("commas_only_sep", ",,0,,1,,\n", {}, ("text", "file")),
+    ("err_tokens", "0 1\n2\n3 4\n", {}, ("text", "file")),
+    ("err_tokens_commas", "0 1\n,,,\n", {}, ("text", "file")),
+    ("err_nonint", "0 1\n1 x\n", {}, ("text", "file")),
+    ("err_float", "0 1.5\n", {}, ("text", "file")),
+    ("err_underscore", "1_ 2\n", {}, ("text", "file")),
+    ("err_double_underscore", "1__0 2\n", {}, ("text", "file")),
+    ("err_first_of_two", "0 1\na b\nc\n", {}, ("text", "file")),
+    ("err_nul", "0\x001\n", {}, ("text", "file")),
+    ("err_empty", "", {}, ("text", "file")),
+    ("err_comments_only", "# a\n% b\n\n", {}, ("text", "file")),
+    ("mm_header", "%%MatrixMarket matrix coordinate pattern symmetric\n% c\n5 5 3\n1 2\n2 3\n3 1\n",
+     {}, ("text", "file")),
+    ("mm_no_header", "%%MatrixMarket matrix coordinate pattern\n1 2\n2 3\n", {}, ("text", "file")),
+    ("mm_out_of_range", "%%MatrixMarket x\n3 3 2\n1 4\n", {}, ("text", "file")),
+    ("mm_zero_id", "%%MatrixMarket x\n3 3 2\n0 2\n", {}, ("text", "file")),
+    ("mm_bad_header", "%%MatrixMarket x\n3 x 2\n1 2\n", {}, ("text", "file")),
+    ("mm_num_vertices", "%%MatrixMarket x\n4 4 2\n1 2\n2 3\n", {"num_vertices": 10}, ("text",)),
+    ("mm_use_max_id", "%%MatrixMarket x\n4 4 2\n1 2\n2 3\n", {"use_max_id": True}, ("text",)),
+    ("mm_after_data", "0 1\n%%MatrixMarket\n3 3 3\n", {}, ("text",)),
+    ("mm_custom_prefix", "%%MatrixMarket x\n2 2 1\n1 2\n", {"comment_prefixes": ["#"]}, ("text",)),
+    ("custom_prefix", "// c\n0 1\n", {"comment_prefixes": ["//"]}, ("text",)),
+    ("custom_prefix_hash_data", "# c\n0 1\n", {"comment_prefixes": ["//"]}, ("text",)),
+    ("empty_prefix", "0 1\n", {"comment_prefixes": [""]}, ("text",)),
+    ("declared_n", "0 1\n2 3\n", {"num_vertices": 10}, ("text",)),
+    ("declared_out_of_range", "0 1\n12 3\n", {"num_vertices": 10}, ("text",)),
+    ("use_max_id", "0 5\n", {"use_max_id": True}, ("text",)),
+    ("unicode_digit", "0 1\n١ 2\n", {}, ("text", "file")),
+    ("unicode_space", "0\u00a01\n2\u20033\n", {}, ("text", "file")),
+    ("overflow", "99999999999999999999 1\n", {}, ("text",)),
+    ("overflow_then_error", "99999999999999999999 1\nx y\n", {}, ("text",)),
+]
+
+
+def _random_edge_text(seed: int, lines: int) -> str:
+    rng = np.random.default_rng(seed)
+    seps = [" ", "\t", ",", " , ", "  "]
+    out = []
+    for i in range(lines):
+        r = rng.random()
+        if r < 0.05:
+            out.append("# comment %d" % i)
+        elif r < 0.08:
+            out.append("")
+        else:
+            u, v = rng.integers(0, 300, size=2)
+            line = f"{u}{seps[rng.integers(0, len(seps))]}{v}"
+            if rng.random() < 0.2:
+                line += f" {rng.integers(0, 9)}"
+            if rng.random() < 0.1:
+                line = "  " + line + " \t"
+            out.append(line)
+    return "\n".join(out) + "\n"
+
+
+PARSE_CASES.append(("random_2000", _random_edge_text(7, 2000), {}, ("text", "file")))
+PARSE_CASES.append(("random_2000_crlf", _random_edge_text(8, 2000).replace("\n", "\r\n"), {},
+                    ("text", "file")))
+
+
+def make_parse():
+    """Reference Graph.from_text / Graph.from_file on edge-list texts covering
+    its parsing rules and error messages (graph.py:223-285)."""
+    import tempfile
+    out = []
+    for name, text, opts, modes in PARSE_CASES:
+        o = dict(opts)
+        if "comment_prefixes" in o:
+            o["comment_prefixes"] = tuple(o["comment_prefixes"])
+        for mode in modes:
+            try:
+                if mode == "text":
+                    g = R.Graph.from_text(text, R.ParseOptions(**o))
+                else:
+                    with tempfile.NamedTemporaryFile("wb", suffix=".txt", delete=False) as fh:
+                        fh.write(text.encode("utf-8"))
+                    try:
+                        g = R.Graph.from_file(fh.name, R.ParseOptions(**o))
+                    finally:
+                        os.unlink(fh.name)
+                res = {"n": g.n, "edges": g.edges.tolist(), "orig_ids": [str(x) for x in g.orig_ids]}
+            except Exception as exc:  # noqa: BLE001
+                res = {"error": type(exc).__name__, "message": str(exc),
+                       "line": getattr(exc, "line", None)}
+            out.append({"name": name, "mode": mode, "text": text, "opts": opts, **res})
+    (HERE / "parse_cases.json").write_text(json.dumps(out, indent=0))
+    print("parse cases:", len(out))
+
+
+if __name__ == "__main__" and "--parse" in sys.argv:
+    make_parse()
