@@ -71,7 +71,7 @@ SIGNATURES = (
     ("gd_host_free", None, [_vp]),
     ("gd_flush_l2", ctypes.c_int, []),
     ("gd_trim_workspace", ctypes.c_int, []),
-    ("gd_parse_edge_list", ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64,
+    ("gd_parse_edge_list", ctypes.c_int, [_vp, ctypes.c_int64,
                                           ctypes.POINTER(ctypes.c_char_p), ctypes.c_int,
                                           ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
     ("gd_parsed_info", ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int64)]),

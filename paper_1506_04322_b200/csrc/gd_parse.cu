@@ -84,18 +84,27 @@ __host__ __device__ __forceinline__ bool starts_with(const unsigned char* s, int
   return true;
 }
 
-// Byte flags: '\n' positions, and input the ASCII rules cannot decide.
+// Input the ASCII rules cannot decide, and the number of '\n' bytes.
 __global__ void k_scan_bytes(const unsigned char* __restrict__ buf, int64_t len, int cr_newline,
-                             unsigned char* __restrict__ nl, int* __restrict__ fallback) {
+                             unsigned long long* __restrict__ nnl, int* __restrict__ fallback) {
+  unsigned cnt = 0;
+  bool odd = false;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
        i += (int64_t)gridDim.x * blockDim.x) {
     const unsigned char c = buf[i];
-    nl[i] = c == '\n';
-    bool odd = c >= 0x80;
+    cnt += c == '\n';
+    odd |= c >= 0x80;
     if (c == '\r' && cr_newline && (i + 1 == len || buf[i + 1] != '\n')) odd = true;
-    if (odd) atomicOr(fallback, 1);
   }
+  for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(nnl, (unsigned long long)cnt);
+  if (odd) atomicOr(fallback, 1);
 }
+
+struct IsNewline {
+  const unsigned char* buf;
+  __device__ __forceinline__ bool operator()(int64_t i) const { return buf[i] == '\n'; }
+};
 
 enum LineKind : unsigned char { kSkip = 0, kData = 1 };
 // error kinds (reported as (line << 2) | kind, minimum over lines)
@@ -285,29 +294,41 @@ void parse_edge_list(const char* text, int64_t len, const char* const* prefixes,
   }
   out.info[1] = pre.mm_rows;
   // bytes to the device; '\n' positions
-  DBuf<unsigned char> dbuf, nl;
+  DBuf<unsigned char> dbuf;
   dbuf.alloc(len, s);
-  nl.alloc(len, s);
   GD_CUDA(cudaMemcpyAsync(dbuf.p, text, len, cudaMemcpyHostToDevice, s));
   DBuf<int> dflag;
+  DBuf<unsigned long long> dnnl;
   dflag.alloc(1, s);
   dflag.zero();
-  k_scan_bytes<<<grid_for(len), 256, 0, s>>>(dbuf.p, len, cr_newline, nl.p, dflag.p);
-  GD_LAUNCH_CHECK("parse_scan_bytes");
-  DBuf<int64_t> nlpos, nsel;
-  nlpos.alloc(len + 1, s);
-  nsel.alloc(1, s);
-  {
-    cub::CountingInputIterator<int64_t> it(0);
-    size_t tb = 0;
-    GD_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, nl.p, nlpos.p, nsel.p, len, s));
-    DBuf<char> tmp;
-    tmp.alloc(tb, s);
-    GD_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, it, nl.p, nlpos.p, nsel.p, len, s));
+  dnnl.alloc(1, s);
+  dnnl.zero();
+  if (len) {
+    k_scan_bytes<<<grid_for(len), 256, 0, s>>>(dbuf.p, len, cr_newline, dnnl.p, dflag.p);
+    GD_LAUNCH_CHECK("parse_scan_bytes");
   }
   int64_t nnl = 0;
-  GD_CUDA(cudaMemcpyAsync(&nnl, nsel.p, 8, cudaMemcpyDeviceToHost, s));
+  int hflag0 = 0;
+  GD_CUDA(cudaMemcpyAsync(&nnl, dnnl.p, 8, cudaMemcpyDeviceToHost, s));
+  GD_CUDA(cudaMemcpyAsync(&hflag0, dflag.p, 4, cudaMemcpyDeviceToHost, s));
   GD_CUDA(cudaStreamSynchronize(s));
+  if (hflag0) {
+    out.info[6] = hflag0;
+    return;
+  }
+  // '\n' positions (exact size; one more slot for an unterminated last line)
+  DBuf<int64_t> nlpos, nsel;
+  nlpos.alloc(nnl + 1, s);
+  nsel.alloc(1, s);
+  if (nnl) {
+    cub::CountingInputIterator<int64_t> it(0);
+    IsNewline pred{dbuf.p};
+    size_t tb = 0;
+    GD_CUDA(cub::DeviceSelect::If(nullptr, tb, it, nlpos.p, nsel.p, len, pred, s));
+    DBuf<char> tmp;
+    tmp.alloc(tb, s);
+    GD_CUDA(cub::DeviceSelect::If(tmp.p, tb, it, nlpos.p, nsel.p, len, pred, s));
+  }
   // lines: one per '\n', plus a last unterminated one
   const bool tail = len > 0 && hb[len - 1] != '\n';
   const int64_t nlines = nnl + (tail ? 1 : 0);

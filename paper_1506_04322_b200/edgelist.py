@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes
 import io
+import sys
 from pathlib import Path
 from typing import IO, Iterable
 
@@ -56,8 +57,26 @@ def _device_prefixes(options: ParseOptions):
     return enc
 
 
-def _parse_device(data: bytes, options: ParseOptions, cr_newline: bool) -> Graph | None:
-    """Parse `data` on the GPU; None when the input needs CPython's rules."""
+_ASCII_OFFSET = sys.getsizeof("") - 1  # CPython: compact ASCII str data offset
+
+
+def _ascii_view(text: str):
+    """(address, length) of the bytes of an ASCII str without copying them
+    (CPython stores such strings as one byte per character right after the
+    object header); verified against the string, else None."""
+    if sys.implementation.name != "cpython" or not text.isascii():
+        return None
+    addr = id(text) + _ASCII_OFFSET
+    k = min(len(text), 64)
+    if ctypes.string_at(addr, k) != text[:k].encode("ascii") or \
+            ctypes.string_at(addr + len(text) - k, k) != text[len(text) - k:].encode("ascii"):
+        return None
+    return addr, len(text)
+
+
+def _parse_device(data, options: ParseOptions, cr_newline: bool, keep=None) -> Graph | None:
+    """Parse `data` (bytes, or an (address, length) view of `keep`) on the
+    GPU; None when the input needs CPython's rules."""
     enc = _device_prefixes(options)
     if enc is None:
         return None
@@ -67,7 +86,8 @@ def _parse_device(data: bytes, options: ParseOptions, cr_newline: bool) -> Graph
     mm_shift = options.num_vertices is None and not options.use_max_id
     flags = (N.GD_PARSE_CR_NEWLINE if cr_newline else 0) | (N.GD_PARSE_MM_SHIFT if mm_shift else 0)
     h = ctypes.c_void_p()
-    N.check(L.gd_parse_edge_list(data, len(data), arr, len(enc), flags, ctypes.byref(h)))
+    ptr, size = data if isinstance(data, tuple) else (data, len(data))
+    N.check(L.gd_parse_edge_list(ptr, size, arr, len(enc), flags, ctypes.byref(h)))
     global last_route
     try:
         info = (ctypes.c_int64 * 12)()
@@ -77,7 +97,8 @@ def _parse_device(data: bytes, options: ParseOptions, cr_newline: bool) -> Graph
             return None
         last_route = "device"
         if kind:
-            text = data[off:off + ln].decode("ascii").strip() if kind in (1, 2) else ""
+            raw = ctypes.string_at(ptr + off, ln) if isinstance(ptr, int) else ptr[off:off + ln]
+            text = raw.decode("ascii").strip() if kind in (1, 2) else ""
             if kind == _ERR_TOKENS:
                 raise EdgeListParseError(f"expected at least 2 integer tokens, got {text!r}", line)
             if kind == _ERR_NONINT:
@@ -181,7 +202,10 @@ def load_edge_list(source: IO[str] | Iterable[str], options: ParseOptions | None
 def from_text(text: str, options: ParseOptions | None = None) -> Graph:
     """Graph.from_text (graph.py:164-166): lines split on '\\n' only."""
     options = options or ParseOptions()
-    g = _parse_device(text.encode("ascii"), options, cr_newline=False) if text.isascii() else None
+    view = _ascii_view(text)
+    if view is None and text.isascii():
+        view = text.encode("ascii")
+    g = _parse_device(view, options, cr_newline=False) if view is not None else None
     return g if g is not None else _load_lines(io.StringIO(text), options)
 
 

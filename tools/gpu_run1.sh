@@ -1,3 +1,2 @@
-timeout 900 python -m pytest tests/ -m gpu -x -q > gpurun_out/t_all.log 2>&1; echo rc=$? >> gpurun_out/t_all.log
-timeout 600 python tools/e2e_breakdown.py c3_rmat20 > gpurun_out/e2e.log 2>&1
-timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_r01.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_edgelist.py -x -q -s > gpurun_out/t_parse.log 2>&1; echo rc=$? >> gpurun_out/t_parse.log
+timeout 900 python tools/time_parse.py c3_rmat20 > gpurun_out/time_parse.log 2>&1
