@@ -213,6 +213,29 @@ GD_API int gd_parsed_info(const gd_parsed* p, int64_t* info);
 GD_API const int64_t* gd_parsed_pairs(const gd_parsed* p);
 GD_API void gd_parsed_free(gd_parsed* p);
 
+/*
+ * Derived per-edge outputs on the device.  `table` is
+ * the [m][10] micro table of `g` (device memory with GD_INPUT_DEVICE),
+ * `orig_ids` the host int64 [n] original vertex ids.
+ * gd_micro_roles replaces _derive_micro over all edges (census.py:574-596):
+ * roles = int64 [m][15] in the order tt1 tt0 susv1 susv0 ts1 ts0 ss1 ss0
+ * ti1 ti0 si1 si0 ii1 ii0 indep3.
+ * gd_micro_csv replaces micro_csv (census.py:603-623): the CSV text
+ * (header + one row per edge, original ids) in a device buffer, read with
+ * gd_text_size / gd_text_copy.
+ * A negative derived count returns GD_ECONSISTENCY and sets *bad to
+ * (edge << 4 | k), k indexing tt0 susv0 ts0 ss0 ti0 ti1 si0 si1 ii0 ii1 (the
+ * reference's check order); *bad = -1 otherwise.
+ */
+typedef struct gd_text gd_text;
+GD_API int gd_micro_roles(const gd_graph* g, const int64_t* table, int flags,
+                          const int64_t* orig_ids, int64_t* roles, int64_t* bad);
+GD_API int gd_micro_csv(const gd_graph* g, const int64_t* table, int flags,
+                        const int64_t* orig_ids, gd_text** out, int64_t* bad);
+GD_API int64_t gd_text_size(const gd_text* t);
+GD_API int gd_text_copy(const gd_text* t, int64_t offset, int64_t len, char* host);
+GD_API void gd_text_free(gd_text* t);
+
 /* Write a buffer larger than L2 on the library stream (timing hygiene). */
 GD_API int gd_flush_l2(void);
 

@@ -23,6 +23,7 @@ from .introspect import (clear_marks, clique_count, cycle_count, edge_neighborho
                          same_side_star_edges)
 from .micro import (MICRO_CSV_HEADER, EdgeLocalCounts, MicroCounts, UnrestrictedCounts,
                     derive_micro, micro_census, micro_counts_from_table, micro_csv,
+                    micro_roles, write_micro_csv, ROLE_COLUMNS,
                     unrestricted_counts)
 from .parallel import MAX_BATCH_SIZE, ParallelConfig, WorkerFailure
 
@@ -43,6 +44,7 @@ __all__ = [
     "MAX_BATCH_SIZE", "ParallelConfig", "WorkerFailure",
     "MICRO_CSV_HEADER", "EdgeLocalCounts", "MicroCounts", "UnrestrictedCounts", "derive_micro",
     "micro_census", "micro_counts_from_table", "micro_csv", "unrestricted_counts",
+    "micro_roles", "write_micro_csv", "ROLE_COLUMNS",
     "clear_marks", "clique_count", "cycle_count", "edge_neighborhood_census",
     "same_side_star_edges",
     "__version__",

@@ -77,6 +77,13 @@ SIGNATURES = (
     ("gd_parsed_info", ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int64)]),
     ("gd_parsed_pairs", _vp, [_vp]),
     ("gd_parsed_free", None, [_vp]),
+    ("gd_micro_roles", ctypes.c_int, [_vp, _vp, ctypes.c_int, _vp, _vp,
+                                      ctypes.POINTER(ctypes.c_int64)]),
+    ("gd_micro_csv", ctypes.c_int, [_vp, _vp, ctypes.c_int, _vp, ctypes.POINTER(ctypes.c_void_p),
+                                    ctypes.POINTER(ctypes.c_int64)]),
+    ("gd_text_size", ctypes.c_int64, [_vp]),
+    ("gd_text_copy", ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, _vp]),
+    ("gd_text_free", None, [_vp]),
 )
 
 

@@ -8,6 +8,7 @@
 #include "gd_build.cuh"
 #include "gd_count.cuh"
 #include "gd_parse.cuh"
+#include "gd_derive.cuh"
 
 struct gd_graph {
   gd::DevGraph g;
@@ -599,6 +600,72 @@ void gd_parsed_free(gd_parsed* p) {
   if (!p) return;
   if (p->out.pairs.p) cudaStreamSynchronize(p->out.pairs.s);
   delete p;
+}
+
+static const char* kNegNames[10] = {"tt0", "susv0", "ts0", "ss0", "ti0",
+                                    "ti1", "si0", "si1", "ii0", "ii1"};
+
+static void set_bad(int64_t hb, int64_t* bad) {
+  if (bad) *bad = hb;
+  if (hb >= 0)
+    throw Error(GD_ECONSISTENCY, std::string("negative micro count ") + kNegNames[hb & 15] +
+                                     " on edge " + std::to_string(hb >> 4));
+}
+
+int gd_micro_roles(const gd_graph* h, const int64_t* table, int flags, const int64_t* orig_ids,
+                   int64_t* roles, int64_t* bad) {
+  if (!h || (h->g.m && (!table || !roles)) || (h->g.n && !orig_ids)) {
+    t_last_error = "NULL argument";
+    return GD_EINVAL;
+  }
+  return guarded([&] {
+    const int64_t hb = micro_roles(h->g, (const long long*)table, (flags & GD_INPUT_DEVICE) != 0,
+                                   orig_ids, (long long*)roles, thread_stream());
+    set_bad(hb, bad);
+  });
+}
+
+struct gd_text {
+  gd::CsvText csv;
+};
+
+int gd_micro_csv(const gd_graph* h, const int64_t* table, int flags, const int64_t* orig_ids,
+                 gd_text** out, int64_t* bad) {
+  if (!h || !out || (h->g.m && !table) || (h->g.n && !orig_ids)) {
+    t_last_error = "NULL argument";
+    return GD_EINVAL;
+  }
+  *out = nullptr;
+  gd_text* t = new gd_text();
+  const int rc = guarded([&] {
+    const int64_t hb = micro_csv(h->g, (const long long*)table, (flags & GD_INPUT_DEVICE) != 0,
+                                 orig_ids, t->csv, thread_stream());
+    set_bad(hb, bad);
+  });
+  if (rc != GD_OK) {
+    delete t;
+    return rc;
+  }
+  *out = t;
+  return GD_OK;
+}
+
+int64_t gd_text_size(const gd_text* t) { return t ? t->csv.bytes : 0; }
+
+int gd_text_copy(const gd_text* t, int64_t offset, int64_t len, char* host) {
+  if (!t || offset < 0 || len < 0 || offset + len > t->csv.bytes || (len && !host)) {
+    t_last_error = "bad text range";
+    return GD_EINVAL;
+  }
+  return guarded([&] {
+    if (len) GD_CUDA(cudaMemcpy(host, t->csv.text.p + offset, len, cudaMemcpyDeviceToHost));
+  });
+}
+
+void gd_text_free(gd_text* t) {
+  if (!t) return;
+  if (t->csv.text.p) cudaStreamSynchronize(t->csv.text.s);
+  delete t;
 }
 
 int gd_trim_workspace(void) {

@@ -8,8 +8,7 @@ nothing here counts graphlets on the CPU.
 
 from __future__ import annotations
 
-import csv
-import io
+import ctypes
 from dataclasses import dataclass
 from math import comb
 
@@ -147,15 +146,87 @@ MICRO_CSV_HEADER = [
 ]
 
 
+ROLE_COLUMNS = ("tt1", "tt0", "susv1", "susv0", "ts1", "ts0", "ss1", "ss0", "ti1", "ti0",
+                "si1", "si0", "ii1", "ii0", "indep3")
+_NEG_ORDER = ("tt0", "susv0", "ts0", "ss0", "ti0", "ti1", "si0", "si1", "ii0", "ii1")
+
+
+def _device_args(g, table):
+    """Our device graph for `g` (any object with n, edges, orig_ids) and the
+    table as a C-contiguous int64 (m, 10) array."""
+    from .graph import Graph
+    dg = Graph.from_reference(g)
+    tab = np.ascontiguousarray(table, dtype=np.int64)
+    if tab.shape != (dg.m, 10):
+        raise ValueError(f"table must have shape ({dg.m}, 10)")
+    orig = np.ascontiguousarray(g.orig_ids if hasattr(g, "orig_ids") else dg.orig_ids,
+                                dtype=np.int64)
+    return dg, tab, orig
+
+
+def _raise_negative(g, bad: int) -> None:
+    idx, k = bad >> 4, bad & 15
+    u, v = (int(x) for x in np.asarray(g.edges)[idx])
+    raise ConsistencyError(f"negative micro count {_NEG_ORDER[k]} on edge {EdgeRef(idx, u, v)}")
+
+
+def micro_roles(g, table: np.ndarray) -> np.ndarray:
+    """_derive_micro over every edge on the device (census.py:574-596):
+    int64 (m, 15) in ROLE_COLUMNS order.  ConsistencyError as the reference."""
+    from . import _native as N
+    dg, tab, orig = _device_args(g, table)
+    out = np.empty((dg.m, len(ROLE_COLUMNS)), dtype=np.int64)
+    bad = ctypes.c_int64(-1)
+    rc = N.lib().gd_micro_roles(dg.handle, N.vptr(tab), 0, N.vptr(orig), N.vptr(out),
+                                ctypes.byref(bad))
+    if bad.value >= 0:
+        _raise_negative(g, bad.value)
+    N.check(rc)
+    return out
+
+
+class _Text:
+    """A device CSV buffer (gd_micro_csv)."""
+
+    def __init__(self, g, table):
+        from . import _native as N
+        self.N, self.L = N, N.lib()
+        dg, tab, orig = _device_args(g, table)
+        self.h = ctypes.c_void_p()
+        bad = ctypes.c_int64(-1)
+        rc = self.L.gd_micro_csv(dg.handle, N.vptr(tab), 0, N.vptr(orig), ctypes.byref(self.h),
+                                 ctypes.byref(bad))
+        if bad.value >= 0:
+            _raise_negative(g, bad.value)
+        N.check(rc)
+        self.size = int(self.L.gd_text_size(self.h))
+
+    def read(self, offset: int, length: int) -> bytearray:
+        buf = bytearray(length)
+        if length:
+            view = (ctypes.c_char * length).from_buffer(buf)
+            self.N.check(self.L.gd_text_copy(self.h, offset, length, view))
+            del view
+        return buf
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value:
+            self.L.gd_text_free(self.h)
+            self.h = None
+
+
 def micro_csv(g, table: np.ndarray) -> str:
-    """Per-edge role CSV with original vertex ids (census.py:603-623)."""
-    orig = np.asarray(g.orig_ids)[np.asarray(g.edges)]
-    buf = io.StringIO()
-    w = csv.writer(buf, lineterminator="\n")
-    w.writerow(MICRO_CSV_HEADER)
-    for i in range(int(g.m)):
-        mc = micro_counts_from_table(g, table, i)
-        w.writerow([int(orig[i, 0]), int(orig[i, 1]), mc.local.tri, mc.local.star_u,
-                    mc.local.star_v, mc.tt1, mc.susv1, mc.tt0, mc.susv0, mc.ts1, mc.ss1,
-                    mc.ss0, mc.ti1, mc.ti0, mc.si1, mc.si0, mc.ii1, mc.ii0, mc.local.indep3])
-    return buf.getvalue()
+    """Per-edge role CSV with original vertex ids (census.py:603-623),
+    derived and formatted on the device."""
+    t = _Text(g, table)
+    return t.read(0, t.size).decode("ascii")
+
+
+def write_micro_csv(g, table: np.ndarray, path, chunk: int = 256 << 20) -> int:
+    """Stream micro_csv(g, table) into a file without building the string;
+    returns the bytes written."""
+    t = _Text(g, table)
+    with open(path, "wb") as fh:
+        for off in range(0, t.size, chunk):
+            fh.write(t.read(off, min(chunk, t.size - off)))
+    return t.size

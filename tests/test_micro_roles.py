@@ -28,11 +28,39 @@ def test_derive_micro_matches_reference_roles():
             gd.unrestricted_counts(mc.local, g.n, g.m, micro=mc)
 
 
-def test_micro_csv_matches_reference():
-    for c in _load()["graphs"]:
+def test_oracle_micro_csv_and_roles_match_reference():
+    """The oracle restatement (checker of the device derive) is pinned to the
+    reference's MicroCounts and CSV text."""
+    from oracle import micro_oracle as MO
+    d = _load()
+    for c in d["graphs"]:
+        tab = np.asarray(c["micro"], dtype=np.int64)
+        assert MO.micro_csv(c["n"], c["edges"], c["orig_ids"], tab) == c["csv"], c["name"]
+        roles = MO.roles_table(c["n"], len(c["edges"]), tab)
+        assert roles.tolist() == [r for r in c["roles"]], c["name"]
+
+
+@pytest.mark.gpu
+def test_device_micro_csv_and_roles_match_reference():
+    d = _load()
+    for c in d["graphs"]:
         g = SimpleNamespace(n=c["n"], m=len(c["edges"]), edges=np.asarray(c["edges"]),
                             orig_ids=np.asarray(c["orig_ids"]))
-        assert gd.micro_csv(g, np.asarray(c["micro"], dtype=np.int64)) == c["csv"], c["name"]
+        tab = np.asarray(c["micro"], dtype=np.int64)
+        assert gd.micro_csv(g, tab) == c["csv"], c["name"]
+        assert gd.micro_roles(g, tab).tolist() == c["roles"], c["name"]
+
+
+@pytest.mark.gpu
+def test_device_negative_role_raises_reference_message():
+    g = gd.Graph(4, np.asarray([[0, 1], [1, 2]]))
+    tab = np.zeros((2, 10), dtype=np.int64)
+    tab[1] = [2, 0, 0, 5, 0, 0, 0, 0, 0, 0]  # cl > C(t, 2) on edge 1
+    with pytest.raises(gd.ConsistencyError) as ei:
+        gd.micro_csv(g, tab)
+    assert str(ei.value) == "negative micro count tt0 on edge EdgeRef(index=1, u=1, v=2)"
+    with pytest.raises(gd.ConsistencyError):
+        gd.micro_roles(g, tab)
 
 
 def test_negative_role_is_consistency_error():
