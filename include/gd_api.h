@@ -236,6 +236,25 @@ GD_API int64_t gd_text_size(const gd_text* t);
 GD_API int gd_text_copy(const gd_text* t, int64_t offset, int64_t len, char* host);
 GD_API void gd_text_free(gd_text* t);
 
+/*
+ * Edge analytics over the per-edge table (analytics.py:
+ * 142-194).  Patterns: GD_PATTERN_* (weights: triangle = t, clique4 = cl,
+ * cycle4 = cy, star4 = C(su,2) + C(sv,2) - uu - vv).  `table` is the [m][10]
+ * micro table (device memory with GD_INPUT_DEVICE); outputs are host arrays.
+ * gd_rank_edges writes the top `k` edges (k < 0: all) by descending weight,
+ * canonical index breaking ties: index, dense endpoints u < v, weight.
+ */
+#define GD_PATTERN_TRIANGLE 0
+#define GD_PATTERN_CLIQUE4  1
+#define GD_PATTERN_CYCLE4   2
+#define GD_PATTERN_STAR4    3
+GD_API int gd_edge_weights(const gd_graph* g, const int64_t* table, int flags, int pattern,
+                           int64_t* weights);
+GD_API int gd_rank_edges(const gd_graph* g, const int64_t* table, int flags, int pattern,
+                         int64_t k, int64_t* index, int64_t* u, int64_t* v, int64_t* weight);
+GD_API int gd_vertex_triangles(const gd_graph* g, const int64_t* table, int flags,
+                               int64_t* per_vertex);
+
 /* Write a buffer larger than L2 on the library stream (timing hygiene). */
 GD_API int gd_flush_l2(void);
 

@@ -7,7 +7,8 @@ running as hand-written sm_100a kernels in libgdgpu.so (C ABI:
 include/gd_api.h).  There is no CPU fallback.
 """
 
-from .analytics import FeatureMatrix, GfdVector, feature_matrix, gfd
+from .analytics import (RANK_PATTERNS, FeatureMatrix, GfdVector, RankedEdge, edge_weights,
+                        feature_matrix, gfd, rank_edges, vertex_triangle_counts)
 from .census import (RAW_MICRO_FIELDS, CensusSums, census_batch, close_quads,
                      close_triads, frequencies_from_micro, frequencies_from_sums,
                      graphlet_census, last_stats, last_timings, micro_census_table,
@@ -31,6 +32,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "FeatureMatrix", "GfdVector", "feature_matrix", "gfd",
+    "RANK_PATTERNS", "RankedEdge", "edge_weights", "rank_edges", "vertex_triangle_counts",
     "RAW_MICRO_FIELDS", "CensusSums", "census_batch", "close_quads", "close_triads",
     "frequencies_from_micro", "frequencies_from_sums", "graphlet_census", "last_stats",
     "last_timings", "micro_census_table", "micro_table", "trim_workspace",

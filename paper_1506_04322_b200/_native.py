@@ -84,6 +84,10 @@ SIGNATURES = (
     ("gd_text_size", ctypes.c_int64, [_vp]),
     ("gd_text_copy", ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, _vp]),
     ("gd_text_free", None, [_vp]),
+    ("gd_edge_weights", ctypes.c_int, [_vp, _vp, ctypes.c_int, ctypes.c_int, _vp]),
+    ("gd_rank_edges", ctypes.c_int, [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
+                                     _vp, _vp, _vp, _vp]),
+    ("gd_vertex_triangles", ctypes.c_int, [_vp, _vp, ctypes.c_int, _vp]),
 )
 
 

@@ -132,3 +132,100 @@ def feature_matrix(graphs, labels=None, config: ParallelConfig | None = None,
 
 
 __all__ = ["GfdVector", "gfd", "FeatureMatrix", "feature_matrix", "graphlet_census"]
+
+
+# ---------------------------------------------------------------------------
+# edge analytics over the per-edge table (analytics.py:134-194)
+# ---------------------------------------------------------------------------
+RANK_PATTERNS = ("star4", "clique4", "triangle", "cycle4")
+_PATTERN_CODE = {"triangle": 0, "clique4": 1, "cycle4": 2, "star4": 3}
+
+
+@dataclass(frozen=True)
+class RankedEdge:
+    index: int
+    u: int            # original ids
+    v: int
+    weight: int
+
+
+class _TableArg:
+    """The micro table for an analytics call: the caller's host table, or a
+    fresh device table from the per-edge census (never copied to the host)."""
+
+    def __init__(self, g, table, config):
+        from . import _native as N
+        from .census import micro_census_table
+        from .graph import Graph
+        self.N = N
+        self.g = Graph.from_reference(g)
+        self.dev = None
+        if table is not None:
+            self.host = np.ascontiguousarray(table, dtype=np.int64)
+            if self.host.shape != (self.g.m, 10):
+                raise ValueError(f"table must have shape ({self.g.m}, 10)")
+            self.ptr, self.flags = N.vptr(self.host), 0
+        elif self.g.m:
+            self.dev = N.lib().gd_device_alloc(self.g.m * 80)
+            if not self.dev:
+                raise MemoryError("device table allocation failed")
+            micro_census_table(self.g, config, device_out=self.dev)
+            self.ptr, self.flags = self.dev, N.GD_INPUT_DEVICE
+        else:
+            self.ptr, self.flags = None, 0
+
+    def close(self):
+        if self.dev:
+            self.N.lib().gd_device_free(self.dev)
+            self.dev = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def _pattern(pattern: str) -> int:
+    if pattern not in RANK_PATTERNS:
+        raise ValueError(f"unknown pattern {pattern!r}; choose from {RANK_PATTERNS}")
+    return _PATTERN_CODE[pattern]
+
+
+def rank_edges(g, pattern: str, top_k: int | None = None, table: np.ndarray | None = None,
+               config: ParallelConfig | None = None) -> list[RankedEdge]:
+    """Edges by descending pattern participation, canonical index breaking
+    ties (analytics.py:142-175); weights and the sort on the device."""
+    from . import _native as N
+    code = _pattern(pattern)
+    with _TableArg(g, table, config) as t:
+        m = t.g.m
+        k = m if top_k is None else max(0, min(int(top_k), m))
+        idx, u, v, w = (np.empty(k, dtype=np.int64) for _ in range(4))
+        N.check(N.lib().gd_rank_edges(t.g.handle, t.ptr, t.flags, code, k, N.vptr(idx),
+                                      N.vptr(u), N.vptr(v), N.vptr(w)))
+    orig = np.asarray(g.orig_ids) if hasattr(g, "orig_ids") else np.asarray(t.g.orig_ids)
+    ou, ov = orig[u], orig[v]
+    return [RankedEdge(index=int(idx[i]), u=int(ou[i]), v=int(ov[i]), weight=int(w[i]))
+            for i in range(k)]
+
+
+def edge_weights(g, pattern: str, table: np.ndarray | None = None,
+                 config: ParallelConfig | None = None) -> np.ndarray:
+    """Per-edge weights in canonical edge order (analytics.py:178-186)."""
+    from . import _native as N
+    code = _pattern(pattern)
+    with _TableArg(g, table, config) as t:
+        out = np.zeros(t.g.m, dtype=np.int64)
+        N.check(N.lib().gd_edge_weights(t.g.handle, t.ptr, t.flags, code, N.vptr(out)))
+    return out
+
+
+def vertex_triangle_counts(g, table: np.ndarray | None = None) -> np.ndarray:
+    """Per-vertex triangle participation (analytics.py:189-194): half the sum
+    of the triangle counts of the incident edges, on the device."""
+    from . import _native as N
+    with _TableArg(g, table, None) as t:
+        out = np.zeros(t.g.n, dtype=np.int64)
+        N.check(N.lib().gd_vertex_triangles(t.g.handle, t.ptr, t.flags, N.vptr(out)))
+    return out

@@ -9,6 +9,7 @@
 #include "gd_count.cuh"
 #include "gd_parse.cuh"
 #include "gd_derive.cuh"
+#include "gd_rank.cuh"
 
 struct gd_graph {
   gd::DevGraph g;
@@ -666,6 +667,49 @@ void gd_text_free(gd_text* t) {
   if (!t) return;
   if (t->csv.text.p) cudaStreamSynchronize(t->csv.text.s);
   delete t;
+}
+
+static bool check_table_args(const gd_graph* h, const int64_t* table, int pattern) {
+  if (!h || (h->g.m && !table)) {
+    t_last_error = "NULL argument";
+    return false;
+  }
+  if (pattern < 0 || pattern > 3) {
+    t_last_error = "unknown pattern";
+    return false;
+  }
+  return true;
+}
+
+int gd_edge_weights(const gd_graph* h, const int64_t* table, int flags, int pattern,
+                    int64_t* weights) {
+  if (!check_table_args(h, table, pattern) || (h->g.m && !weights)) return GD_EINVAL;
+  return guarded([&] {
+    edge_weights(h->g, (const long long*)table, (flags & GD_INPUT_DEVICE) != 0, pattern, weights,
+                 thread_stream());
+  });
+}
+
+int gd_rank_edges(const gd_graph* h, const int64_t* table, int flags, int pattern, int64_t k,
+                  int64_t* index, int64_t* u, int64_t* v, int64_t* weight) {
+  if (!check_table_args(h, table, pattern)) return GD_EINVAL;
+  const int64_t kk = (k < 0 || k > h->g.m) ? h->g.m : k;
+  if (kk && (!index || !u || !v || !weight)) {
+    t_last_error = "NULL output";
+    return GD_EINVAL;
+  }
+  return guarded([&] {
+    rank_edges(h->g, (const long long*)table, (flags & GD_INPUT_DEVICE) != 0, pattern, kk, index,
+               u, v, weight, thread_stream());
+  });
+}
+
+int gd_vertex_triangles(const gd_graph* h, const int64_t* table, int flags, int64_t* per_vertex) {
+  if (!check_table_args(h, table, 0) || (h->g.n && !per_vertex)) return GD_EINVAL;
+  return guarded([&] {
+    vertex_triangles(h->g, (const long long*)table, (flags & GD_INPUT_DEVICE) != 0, per_vertex,
+                     thread_stream());
+  });
 }
 
 int gd_trim_workspace(void) {

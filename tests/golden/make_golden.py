@@ -365,3 +365,36 @@ def make_parse():
 
 if __name__ == "__main__" and "--parse" in sys.argv:
     make_parse()
+
+
+def make_analytics():
+    """Reference rank_edges / edge_weights / vertex_triangle_counts
+    (analytics.py:142-194) on graphs with ties, pendants and remapped ids."""
+    from graphlets.analytics import RANK_PATTERNS, edge_weights, rank_edges, vertex_triangle_counts
+    graphs = [("star5", RG.star_graph(5)), ("k5_pendant", None), ("cycle4", RG.cycle_graph(4)),
+              ("gnp20", RG.gnp_random_graph(20, 0.3, seed=3)),
+              ("gnp40", RG.gnp_random_graph(40, 0.25, seed=11)),
+              ("remapped", R.Graph.from_edges(np.asarray([[100, 200], [200, 300], [300, 100],
+                                                          [300, 4000], [7, 100], [7, 300]])))]
+    out = []
+    for name, g in graphs:
+        if g is None:
+            k5 = [[a, b] for a in range(5) for b in range(a + 1, 5)] + [[4, 5]]
+            g = R.Graph(6, np.asarray(k5))
+        tab = R.micro_table(g)
+        rec = {"name": name, "n": g.n, "edges": g.edges.tolist(),
+               "orig_ids": g.orig_ids.tolist(), "micro": tab.tolist(),
+               "vertex_triangles": vertex_triangle_counts(g, tab).tolist(), "patterns": {}}
+        for p in RANK_PATTERNS:
+            rec["patterns"][p] = {
+                "weights": edge_weights(g, p, table=tab).tolist(),
+                "ranked": [[r.index, int(r.u), int(r.v), int(r.weight)] for r in rank_edges(g, p)],
+                "top3": [[r.index, int(r.u), int(r.v), int(r.weight)]
+                         for r in rank_edges(g, p, top_k=3)]}
+        out.append(rec)
+    (HERE / "analytics.json").write_text(json.dumps(out))
+    print("analytics graphs:", len(out))
+
+
+if __name__ == "__main__" and "--analytics" in sys.argv:
+    make_analytics()
