@@ -255,6 +255,26 @@ GD_API int gd_rank_edges(const gd_graph* g, const int64_t* table, int flags, int
 GD_API int gd_vertex_triangles(const gd_graph* g, const int64_t* table, int flags,
                                int64_t* per_vertex);
 
+/*
+ * Incremental induced-subgraph selections (replaces
+ * SelectionState._refresh_region / _local_tuple / _close, selection.py:
+ * 120-205).  Actions: GD_SEL_ADD_VERTEX / GD_SEL_REMOVE_VERTEX (a = dense
+ * vertex id), GD_SEL_READMIT_EDGE / GD_SEL_EXCLUDE_EDGE (a = canonical edge
+ * id).  The caller applies the reference's validation and no-op rules first.
+ * `moments` receives 11 (lo, hi) two's complement 128-bit running sums over
+ * the selected edges: m_sel, S t, S s, S cl, S cy, S C(t,2), S su*sv, S t*s,
+ * S C(su,2)+C(sv,2), S t^2, S s^2 (s = su + sv), from which the closure of
+ * the selection's census is evaluated (CensusSums with n_sel, m_sel).
+ */
+#define GD_SEL_ADD_VERTEX    0
+#define GD_SEL_REMOVE_VERTEX 1
+#define GD_SEL_READMIT_EDGE  2
+#define GD_SEL_EXCLUDE_EDGE  3
+typedef struct gd_selection gd_selection;
+GD_API int gd_selection_create(const gd_graph* g, gd_selection** out);
+GD_API int gd_selection_apply(gd_selection* s, int action, int64_t a, uint64_t* moments);
+GD_API void gd_selection_free(gd_selection* s);
+
 /* Write a buffer larger than L2 on the library stream (timing hygiene). */
 GD_API int gd_flush_l2(void);
 

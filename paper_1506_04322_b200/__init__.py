@@ -27,6 +27,7 @@ from .micro import (MICRO_CSV_HEADER, EdgeLocalCounts, MicroCounts, Unrestricted
                     micro_roles, write_micro_csv, ROLE_COLUMNS,
                     unrestricted_counts)
 from .parallel import MAX_BATCH_SIZE, ParallelConfig, WorkerFailure
+from .selection import SelectionOp, SelectionState, induced_subgraph, selection_census
 
 __version__ = "0.1.0"
 
@@ -44,6 +45,7 @@ __all__ = [
     "EdgeRef", "Graph", "GraphBatch", "ParseOptions", "order_edges_by_degree",
     "load_edge_list", "to_edge_list_text",
     "MAX_BATCH_SIZE", "ParallelConfig", "WorkerFailure",
+    "SelectionOp", "SelectionState", "induced_subgraph", "selection_census",
     "MICRO_CSV_HEADER", "EdgeLocalCounts", "MicroCounts", "UnrestrictedCounts", "derive_micro",
     "micro_census", "micro_counts_from_table", "micro_csv", "unrestricted_counts",
     "micro_roles", "write_micro_csv", "ROLE_COLUMNS",

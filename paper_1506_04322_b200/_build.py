@@ -12,7 +12,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 BUILD = PKG / "_build_obj"
 LIB = PKG / "libgdgpu.so"
-SOURCES = ("gd_build.cu", "gd_count.cu", "gd_parse.cu", "gd_derive.cu", "gd_rank.cu", "gd_api.cu")
+SOURCES = ("gd_build.cu", "gd_count.cu", "gd_parse.cu", "gd_derive.cu", "gd_rank.cu", "gd_select.cu", "gd_api.cu")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",

@@ -88,6 +88,9 @@ SIGNATURES = (
     ("gd_rank_edges", ctypes.c_int, [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
                                      _vp, _vp, _vp, _vp]),
     ("gd_vertex_triangles", ctypes.c_int, [_vp, _vp, ctypes.c_int, _vp]),
+    ("gd_selection_create", ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_void_p)]),
+    ("gd_selection_apply", ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int64, _vp]),
+    ("gd_selection_free", None, [_vp]),
 )
 
 

@@ -10,6 +10,7 @@
 #include "gd_parse.cuh"
 #include "gd_derive.cuh"
 #include "gd_rank.cuh"
+#include "gd_select.cuh"
 
 struct gd_graph {
   gd::DevGraph g;
@@ -710,6 +711,40 @@ int gd_vertex_triangles(const gd_graph* h, const int64_t* table, int flags, int6
     vertex_triangles(h->g, (const long long*)table, (flags & GD_INPUT_DEVICE) != 0, per_vertex,
                      thread_stream());
   });
+}
+
+struct gd_selection {
+  gd::Selection* sel = nullptr;
+};
+
+int gd_selection_create(const gd_graph* h, gd_selection** out) {
+  if (!h || !out) {
+    t_last_error = "NULL argument";
+    return GD_EINVAL;
+  }
+  *out = nullptr;
+  gd_selection* p = new gd_selection();
+  const int rc = guarded([&] { p->sel = new gd::Selection(h->g, h->s); });
+  if (rc != GD_OK) {
+    delete p;
+    return rc;
+  }
+  *out = p;
+  return GD_OK;
+}
+
+int gd_selection_apply(gd_selection* p, int action, int64_t a, uint64_t* moments) {
+  if (!p || !p->sel) {
+    t_last_error = "NULL selection";
+    return GD_EINVAL;
+  }
+  return guarded([&] { p->sel->apply(action, a, moments); });
+}
+
+void gd_selection_free(gd_selection* p) {
+  if (!p) return;
+  delete p->sel;
+  delete p;
 }
 
 int gd_trim_workspace(void) {

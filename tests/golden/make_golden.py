@@ -398,3 +398,75 @@ def make_analytics():
 
 if __name__ == "__main__" and "--analytics" in sys.argv:
     make_analytics()
+
+
+def make_selection():
+    """Reference SelectionState op streams (selection.py) with the counts
+    after every operation, and the errors of invalid operations."""
+    from graphlets.selection import SelectionOp, SelectionState
+    streams = []
+
+    def run(name, base, ops, active=(), excluded=()):
+        st = SelectionState(base, active=active, excluded_edges=excluded)
+        rec = {"name": name, "n": base.n, "edges": base.edges.tolist(), "active": list(active),
+               "excluded": list(excluded),
+               "initial": {k: str(v) for k, v in st.frequencies().counts.items()}, "steps": []}
+        for op in ops:
+            step = {"op": [op.action, op.vertex, op.u, op.v]}
+            try:
+                f = st.apply_one(op)
+                step["counts"] = {k: str(v) for k, v in f.counts.items()}
+                step["n"], step["m"] = f.n, f.m
+            except Exception as exc:  # noqa: BLE001
+                step["error"] = type(exc).__name__
+            rec["steps"].append(step)
+        streams.append(rec)
+
+    k4 = RG.complete_graph(4)
+    run("k4_build", k4, [SelectionOp("add_vertex", vertex=v) for v in range(4)]
+        + [SelectionOp("add_edge", u=0, v=1), SelectionOp("remove_edge", u=2, v=3),
+           SelectionOp("add_edge", u=2, v=3), SelectionOp("remove_vertex", vertex=3),
+           SelectionOp("remove_vertex", vertex=3), SelectionOp("add_vertex", vertex=99),
+           SelectionOp("remove_edge", u=0, v=0), SelectionOp("teleport", vertex=1),
+           SelectionOp("add_edge", u=0), SelectionOp("remove_edge", u=0, v=1),
+           SelectionOp("remove_vertex", vertex=0), SelectionOp("add_edge", u=0, v=1)])
+    run("k4_excluded_init", k4, [SelectionOp("add_edge", u=2, v=3)], active=[0, 1, 2, 3],
+        excluded=[5])
+
+    def random_stream(name, base, steps, seed):
+        rng = np.random.default_rng(seed)
+        active = set()
+        ops = []
+        for _ in range(steps):
+            kind = int(rng.integers(0, 4))
+            if kind == 0:
+                op = SelectionOp("add_vertex", vertex=int(rng.integers(base.n)))
+            elif kind == 1:
+                op = SelectionOp("remove_vertex", vertex=int(rng.integers(base.n)))
+            else:
+                eid = int(rng.integers(base.m))
+                u, v = (int(x) for x in base.edges[eid])
+                if kind == 2:
+                    op = SelectionOp("remove_edge", u=u, v=v)
+                elif u in active and v in active:
+                    op = SelectionOp("add_edge", u=u, v=v)
+                else:
+                    op = SelectionOp("add_vertex", vertex=u)
+            if op.action == "add_vertex":
+                active.add(op.vertex)
+            elif op.action == "remove_vertex":
+                active.discard(op.vertex)
+            ops.append(op)
+        run(name, base, ops)
+
+    random_stream("random_300", RG.random_graph_avg_degree(300, 8, seed=8), 120, 23)
+    cl = W.chung_lu(1500, 2.1, 10.0, 300.0, seed=31)
+    random_stream("chung_lu_1500", ref_graph(cl), 150, 7)
+    dense = RG.gnp_random_graph(60, 0.5, seed=5)
+    random_stream("gnp60_dense", dense, 200, 9)
+    (HERE / "selection.json").write_text(json.dumps(streams))
+    print("selection streams:", len(streams), sum(len(s["steps"]) for s in streams))
+
+
+if __name__ == "__main__" and "--selection" in sys.argv:
+    make_selection()
