@@ -1,1 +1,2 @@
-timeout 900 python tools/time_derive.py c3_rmat20 > gpurun_out/time_derive.log 2>&1
+timeout 900 python tools/time_selection.py c2_chung_lu > gpurun_out/time_sel.log 2>&1
+timeout 900 python tools/time_selection.py c3_rmat20 >> gpurun_out/time_sel.log 2>&1
