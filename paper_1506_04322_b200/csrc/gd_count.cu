@@ -704,7 +704,11 @@ struct U16Counter {  // dense u16 counters, two per 32-bit word
     atomicAdd(&w[x >> 1], 1u << ((x & 1) << 4));
   }
   __device__ __forceinline__ unsigned get(int x) const {
+#ifdef GD_CNT_CG  // experiment: counter reads bypass L1
+    return __ldcg((const unsigned short*)w + x);
+#else
     return ((const unsigned short*)w)[x];
+#endif
   }
   __device__ __forceinline__ unsigned take(int x) const { return get(x); }  // unused
   __device__ __forceinline__ void zero(int x) const { ((unsigned short*)w)[x] = 0; }
@@ -744,6 +748,12 @@ struct HashCounter {  // shared-memory open-addressing hash, u32 or u16 counts
 // (coalesced).  The slot of the first item is found by one binary search per
 // lane per piece; later rows follow by advancing p (measured: per-512-item
 // searches spent ~40% of the heavy-frame kernel's stalls on that chain).
+// Steps whose U items all lie in the current row (the common case: a
+// wedge-weighted row holds ~360 items at config 3) take a fast path with no
+// per-item slot state: all U col[] loads, then all U counter loads, then the
+// updates, so the dependent counter reads of the use sweep overlap instead of
+// alternating with the per-edge atomics.  Steps that cross a row boundary
+// walk their items one at a time.
 // Returns the thread's partial (kUse: sum of cnt-1; kTake: sum of c*(c-1)).
 template <int NT, int MODE, typename C, int U = 1>
 __device__ __forceinline__ u64 wedge_sweep(const View& g, const int64_t* __restrict__ WP,
@@ -762,51 +772,59 @@ __device__ __forceinline__ u64 wedge_sweep(const View& g, const int64_t* __restr
   int64_t base = g.rp[g.col[p]] - WP[p];  // slot of item i in row w: base + i
   int64_t ptop = p;                       // per-edge: pending sum for slot ptop (edge s-w)
   u64 top = 0;
-  for (; i < c1; i += 32 * U) {
-    int64_t qq[U], pp[U];
-    int xx[U];
-#pragma unroll
-    for (int u = 0; u < U; u++) {  // U items in flight per lane
-      const int64_t ii = i + 32 * u;
-      if (ii < c1 && wp1 <= ii) {
-        do {
-          p++;
-          wp1 = WP[p + 1];
-        } while (wp1 <= ii);
-        base = g.rp[g.col[p]] - WP[p];
-      }
-      qq[u] = base + ii;
-      pp[u] = p;
-    }
-#pragma unroll
-    for (int u = 0; u < U; u++) xx[u] = i + 32 * u < c1 ? __ldg(g.col + qq[u]) : 0;
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      if (i + 32 * u >= c1) continue;
-      const int x = xx[u];
-      if (MODE == kCount) {
-        ctr.inc(x);
-      } else if (MODE == kZero) {
-        ctr.zero(x);
-      } else if (MODE == kTake) {
-        const u64 c = ctr.take(x);
-        local += c * (c - (c > 0));
-      } else {
-        const u64 c = ctr.get(x) - 1u;
-        if (c) {
-          local += c;
-          if (per_edge) {
+  // one item: x = col[q], q its slot, pr its row
+  auto one = [&](int x, int64_t q, int64_t pr, unsigned cnt) {
+    if (MODE == kCount) {
+      ctr.inc(x);
+    } else if (MODE == kZero) {
+      ctr.zero(x);
+    } else if (MODE == kTake) {
+      const u64 c = ctr.take(x);
+      local += c * (c - (c > 0));
+    } else {
+      const u64 c = cnt - 1u;
+      if (c) {
+        local += c;
+        if (per_edge) {
 #ifndef GD_EXP_NO_C4S  // timing experiment only (tools/build_variant.py)
-            atomicAdd(&c4s[qq[u]], c);  // edge w-x
+          atomicAdd(&c4s[q], c);  // edge w-x
 #endif
-            if (pp[u] != ptop) {
-              if (top) atomicAdd(&c4s[ptop], top);
-              top = 0;
-              ptop = pp[u];
-            }
-            top += c;
+          if (pr != ptop) {
+            if (top) atomicAdd(&c4s[ptop], top);
+            top = 0;
+            ptop = pr;
           }
+          top += c;
         }
+      }
+    }
+  };
+  for (; i < c1; i += 32 * U) {
+    const int64_t ilast = i + 32 * (U - 1);
+    if (ilast < c1 && ilast < wp1) {  // all U items in row p
+      const int64_t q0 = base + i;
+      int xx[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) xx[u] = __ldg(g.col + q0 + 32 * u);
+      unsigned cc[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) cc[u] = MODE == kUse ? ctr.get(xx[u]) : 0u;
+#pragma unroll
+      for (int u = 0; u < U; u++) one(xx[u], q0 + 32 * u, p, cc[u]);
+    } else {
+#pragma unroll 1
+      for (int u = 0; u < U; u++) {
+        const int64_t ii = i + 32 * u;
+        if (ii >= c1) break;
+        if (wp1 <= ii) {
+          do {
+            p++;
+            wp1 = WP[p + 1];
+          } while (wp1 <= ii);
+          base = g.rp[g.col[p]] - WP[p];
+        }
+        const int x = __ldg(g.col + base + ii);
+        one(x, base + ii, p, MODE == kUse ? ctr.get(x) : 0u);
       }
     }
   }
@@ -1007,6 +1025,15 @@ __device__ __forceinline__ u64 flow_chunk(const View& g, const int64_t* __restri
   return wedge_sweep<NT, MODE, U16Counter, U>(g, WP, b, o, i0, i1, ctr, per_edge, c4s);
 }
 
+#ifndef GD_FLOW_MINB
+#define GD_FLOW_MINB 4
+#endif
+#ifndef GD_FLOW_U
+#define GD_FLOW_U 2
+#endif
+#ifndef GD_FLOW_UU
+#define GD_FLOW_UU 2
+#endif
 template <int NT, int MINB, int U, int UU>
 __global__ void __launch_bounds__(NT, MINB)
 k_c4_flow(View g, const int64_t* __restrict__ WP, FlowPlan P, unsigned* __restrict__ slabs,
@@ -1815,7 +1842,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       // 4 CTAs/SM (32 registers) and 2 items per lane in flight: measured
       // 72.6 ms vs 87.6 (3 CTAs, 1 item) on config 3; the use sweep's
       // dependent counter reads are latency-bound
-      auto fk = k_c4_flow<NT, 4, 2, 2>;
+      auto fk = k_c4_flow<NT, GD_FLOW_MINB, GD_FLOW_U, GD_FLOW_UU>;
       const int fnt = NT;
       GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fk, fnt, 0));
       if (per_sm < 1) throw Error(GD_ECUDA, "c4 flow kernel cannot be resident");
