@@ -15,6 +15,10 @@
 struct gd_graph {
   gd::DevGraph g;
   cudaStream_t s = nullptr;
+  // censuses of one graph from several host threads run one at a time (the
+  // graph's stream, cached schedule sizes and last timings / stats are
+  // per graph); read-only calls (export, derive, rank) need no lock
+  mutable std::mutex mu;
   std::vector<float> ms;
   std::string names;
   std::vector<int64_t> stats;
@@ -172,6 +176,7 @@ static void store_timings(gd_graph* h, CensusExtras& ex) {
 
 static void census(gd_graph* h, bool per_edge, int64_t* table, int flags, uint64_t* sums,
                    int64_t* seen, const Shard& shard = Shard()) {
+  std::lock_guard<std::mutex> lock(h->mu);
   DevGraph& g = h->g;
   cudaStream_t s = h->s;
   const int64_t G = g.G;
@@ -505,6 +510,7 @@ int gd_close_counts(const uint64_t* sums, const int64_t* n_per_graph, const int6
 
 int gd_graph_timings(const gd_graph* h, float* ms, int capacity, const char** names) {
   if (!h) return 0;
+  std::lock_guard<std::mutex> lock(h->mu);
   int k = (int)std::min<size_t>(h->ms.size(), (size_t)std::max(capacity, 0));
   for (int i = 0; i < k; i++) ms[i] = h->ms[i];
   if (names) *names = h->names.c_str();
@@ -513,6 +519,7 @@ int gd_graph_timings(const gd_graph* h, float* ms, int capacity, const char** na
 
 int gd_graph_stats(const gd_graph* h, int64_t* values, int capacity, const char** names) {
   if (!h) return 0;
+  std::lock_guard<std::mutex> lock(h->mu);
   int k = (int)std::min<size_t>(h->stats.size(), (size_t)std::max(capacity, 0));
   for (int i = 0; i < k; i++) values[i] = h->stats[i];
   if (names) *names = h->stats_names.c_str();

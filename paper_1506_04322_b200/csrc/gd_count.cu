@@ -29,6 +29,8 @@
 // finalize adds both (e2o + e2i).
 #include <algorithm>
 #include <functional>
+#include <map>
+#include <mutex>
 
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
@@ -1440,11 +1442,20 @@ struct Timer {
 };
 
 // Opt in to the dynamic shared memory a launch needs (static shared memory
-// counts against the same 48 KB default, so always set it).
+// counts against the same 48 KB default, so always set it).  The attribute
+// is process-wide per kernel while censuses may run on several host threads
+// at once, so it only ever grows (under a lock): a launch never sees a
+// smaller limit set by a concurrent census of a smaller graph.
 template <typename K>
 void set_smem(K kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<const void*, size_t> cur;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& c = cur[(const void*)kernel];
+  if (bytes <= c) return;
   GD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)bytes));
+  c = bytes;
 }
 
 // Test-only schedule overrides (GD_FORCE_PATH=tri_gmem,c4_coop,...): route
