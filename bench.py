@@ -44,6 +44,9 @@ CONFIG_DESC = {
 }
 
 
+DEBUG = bool(os.environ.get("GD_BENCH_DEBUG"))
+
+
 def dist_env():
     return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
             int(os.environ.get("LOCAL_RANK", "0")))
@@ -337,13 +340,24 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # --- end to end through the public API (host memory both ways) ----------
     dist.barrier()
     e2e_ms = []
-    for i in range(args.steps + 1):
+    # the e2e leg gets the same W untimed warm-up steps as the resident leg
+    # (measured with GD_BENCH_DEBUG=1: the first two fresh graphs after the
+    # resident phase build in 300-450 ms, every later one in 12-17 ms)
+    e2e_warm = max(1, args.warmup)
+    for i in range(args.steps + e2e_warm):
         t0 = time.perf_counter()
         g2 = gd.Graph.from_edges(pairs, gd.ParseOptions(num_vertices=raw.n))
+        tb = time.perf_counter()
         f2 = census(g2, out=htab if per_edge else None)
+        tc = time.perf_counter()
+        dev = sum(gd.last_timings(g2).values()) if DEBUG else 0.0
         del g2
         dt = (time.perf_counter() - t0) * 1e3
-        if i:  # first call is a warm-up of the e2e path
+        if DEBUG:
+            print(f"e2e step {i}: build {1e3 * (tb - t0):.1f} census {1e3 * (tc - tb):.1f} "
+                  f"(device {dev:.1f}) free {1e3 * (time.perf_counter() - tc):.1f}",
+                  file=sys.stderr, flush=True)
+        if i >= e2e_warm:
             e2e_ms.append(dt)
         if f2 != f_ref:
             raise SystemExit("end-to-end census differs from the resident one")
@@ -391,6 +405,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "work": {k: v for k, v in stats.items() if k != "launches"},
             "wall_ms_per_step": wall_ms,
             "e2e": {"value": m / (e2e / 1e3), "unit": "edges/s", "ms_per_step": e2e,
+                    "ms_steps": [round(x, 2) for x in e2e_ms],
                     "h2d_bytes_per_step": int(pairs.nbytes),
                     "d2h_bytes_per_step": int((m * 80 if per_edge else 0) + 13 * 16 + 8)},
             "gpu_launches": launches,

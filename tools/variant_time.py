@@ -1,7 +1,7 @@
 """Time the census under several library builds (GD_LIBRARY variants from
 tools/build_variant.py), each in a subprocess; prints per-phase timings and a
 digest of the counts + per-edge table so variants can be checked against each
-other.  Usage: python tools/variant_time.py CONFIG MODE lib1.so [lib2.so ...]"""
+other.  Usage: python tools/variant_time.py CONFIG MODE lib1.so|default|ENV=VAL ..."""
 import os, subprocess, sys
 cfg, mode, libs = sys.argv[1], sys.argv[2], sys.argv[3:]
 code = r'''
@@ -34,7 +34,10 @@ print(json.dumps({k: round(v, 2) for k, v in tm.items()}), "total_ms %%.2f" %% (
 ''' % (cfg, mode, mode)
 for lib in libs:
     env = dict(os.environ)
-    if lib != "default":
+    if "=" in lib:  # NAME=VALUE: the default library under an env setting
+        k, v = lib.split("=", 1)
+        env[k] = v
+    elif lib != "default":
         env["GD_LIBRARY"] = lib
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     print(os.path.basename(lib), r.stdout.strip()[-500:], r.stderr.strip()[-400:], flush=True)
