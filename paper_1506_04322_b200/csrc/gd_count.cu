@@ -975,11 +975,14 @@ k_c4_cluster(View g, const int64_t* __restrict__ WP, const int* __restrict__ fra
 // rounds of F frames (one dense u16 counter slab each, ranks [x0, n)); a
 // round's wedge items are cut into chunks.  One task sequence is handed out in
 // order by a global counter:
-//   step t:  C(t) count chunks of round t | U(t-1) use chunks (or S(t-1) slab
-//            scans in global mode) | Z(t-2) zeroing of round t-2's slabs
-// with three slab sets (round r uses set r % 3).  A task waits (spins) only
+//   step t:  C(t) count chunks of round t | U(t-LU) use chunks (or S(t-LU)
+//            slab scans in global mode) | Z(t-LU-1) zeroing of that round's slabs
+// with NS >= LU + 2 slab sets (round r uses set r % NS; default LU = 1,
+// NS = 4: a fourth set gives the count tasks of round t a step of slack
+// behind the zeroing they wait for, measured 72.3 -> 65.3 ms at config 3 and
+// 774 -> 692 ms at config 5, per-edge).  A task waits (spins) only
 // on a segment handed out earlier: U(r), S(r) on C(r); Z(r) on U(r); C(t) on
-// the segment that freed its set (Z(t-3) or S(t-3)).  Every awaited task is
+// the segment that freed its set (Z(t-NS) or S(t-NS)).  Every awaited task is
 // therefore already running on a resident CTA, so the kernel needs neither a
 // cooperative launch nor co-residency, and a CTA that finishes early takes
 // the next task instead of idling at a barrier.
@@ -1002,6 +1005,7 @@ struct FlowPlan {
   int64_t slab_words;   // 32-bit words per slab
   int x0;               // first counter (even): counters cover ranks [x0, n)
   int64_t pieces;       // uint4 per fill / scan piece
+  int nsets;            // slab sets (round r uses set r % nsets)
 };
 
 template <int NT, int MODE, int U>
@@ -1069,7 +1073,7 @@ k_c4_flow(View g, const int64_t* __restrict__ WP, FlowPlan P, unsigned* __restri
     __syncthreads();
     const int64_t k = task - sg.task0;
     const int r = sg.round;
-    unsigned* set = slabs + (size_t)(r % 3) * set_words;
+    unsigned* set = slabs + (size_t)(r % P.nsets) * set_words;
     if (sg.type == kFlowCount) {
       int s;
       flow_chunk<NT, kCount, U>(g, WP, P, r, k, set, false, c4s, s);
@@ -1871,9 +1875,14 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
         x0 &= ~1;
       }
       const int64_t slab_words = ((((int64_t)n - x0) + 1) / 2 + 31) & ~int64_t(31);
-      const int64_t l2_budget = env_int("GD_C4_FLOW_MB", 320) << 20;  // three slab sets
+      const int64_t l2_budget = env_int("GD_C4_FLOW_MB", 480) << 20;  // all slab sets
+      // a round's use (or scan) tasks are handed out LU steps after its count
+      // tasks and its zeroing one step later; a count task waits for the
+      // zeroing of the set it reuses, NS rounds back
+      const int LU = (int)std::max<int64_t>(1, env_int("GD_C4_ULAG", 1));
+      const int NS = (int)std::max<int64_t>(LU + 2, env_int("GD_C4_SETS", 4));
       const int F = force.c4_flow ? 2 : (int)std::max<int64_t>(
-          1, std::min<int64_t>(256, l2_budget / (3 * slab_words * 4)));
+          1, std::min<int64_t>(256, l2_budget / (NS * slab_words * 4)));
       const int64_t pieces = force.c4_flow ? 8 : 16384;  // uint4 per fill / scan task
       const int64_t per_slab = (slab_words / 4 + pieces - 1) / pieces;
       const int64_t min_ch = force.c4_flow ? 1 : env_int("GD_C4_MIN_CHUNK", 8192);
@@ -1903,17 +1912,17 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
         task0 += nt;
         return (int)segs.size() - 1;
       };
-      for (int t = 0; t <= R + 1; t++) {
+      for (int t = 0; t <= R + LU; t++) {
         if (t < R)
-          cseg[t] = add(kFlowCount, t, cpre[rf[t + 1]] - cpre[rf[t]], t >= 3 ? freed[t - 3] : -1);
-        const int r1 = t - 1;
+          cseg[t] = add(kFlowCount, t, cpre[rf[t + 1]] - cpre[rf[t]], t >= NS ? freed[t - NS] : -1);
+        const int r1 = t - LU;
         if (r1 >= 0 && r1 < R) {
           const int64_t used = rf[r1 + 1] - rf[r1];
           if (rscan[r1]) freed[r1] = add(kFlowScan, r1, used * per_slab, cseg[r1]);
           else useg[r1] = add(kFlowUse, r1, cpre[rf[r1 + 1]] - cpre[rf[r1]], cseg[r1]);
         }
-        const int r2 = t - 2;
-        if (r2 >= 0 && r2 < R && !rscan[r2] && r2 + 3 < R) {
+        const int r2 = t - LU - 1;
+        if (r2 >= 0 && r2 < R && !rscan[r2] && r2 + NS < R) {
           const int64_t used = rf[r2 + 1] - rf[r2];
           freed[r2] = rzs[r2] ? add(kFlowZeroSweep, r2, cpre[rf[r2 + 1]] - cpre[rf[r2]], useg[r2])
                               : add(kFlowZeroFill, r2, used * per_slab, useg[r2]);
@@ -1938,11 +1947,11 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       GD_CUDA(cudaMemcpyAsync(drch.p, rch.data(), rch.size() * 8, cudaMemcpyHostToDevice, s));
       GD_CUDA(cudaMemcpyAsync(dseg.p, segs.data(), segs.size() * sizeof(FlowSeg),
                               cudaMemcpyHostToDevice, s));
-      const size_t slab_total = (size_t)3 * F * slab_words;
+      const size_t slab_total = (size_t)NS * F * slab_words;
       unsigned* slabs = ws_get<unsigned>(g, "c4_slabs", slab_total, s);
       GD_CUDA(cudaMemsetAsync(slabs, 0, slab_total * 4, s));
       FlowPlan P{dfr.p, dcp.p, drf.p, drch.p, dseg.p, (int)segs.size(), F, slab_words, x0,
-                 pieces};
+                 pieces, NS};
       nrounds += R;
       fk<<<grid, fnt, 0, s>>>(v, WP.p, P, slabs, pe, c4s_p, c4tot2.p, ntask.p, done.p);
       GD_LAUNCH_CHECK("c4_flow");
