@@ -550,11 +550,11 @@ k_tri_frames(View g, const int* __restrict__ frames, int nframes, int rank, int 
 // AccT: the per-base-edge accumulators in shared memory; u32 when
 // D * max_degree < 2^32 (native shared atomics; a 64-bit shared atomicAdd is
 // a CAS loop), u64 otherwise.
-template <int NT, typename AccT>
+template <int NT, typename AccT, typename ST>
 __device__ void trisum_frame(const View& g, int a, char* mem, const FrameLayout& L,
                              const int64_t* __restrict__ OP, const u64* __restrict__ tcs,
-                             u64* __restrict__ tsl, u64* __restrict__ tsh,
-                             u64* __restrict__ tsd, const HitLists& HL) {
+                             ST* __restrict__ tsl, ST* __restrict__ tsh,
+                             ST* __restrict__ tsd, const HitLists& HL) {
   LocalHash H;
   const int D = frame_load<NT>(g, a, mem, L, OP, H);
   const int* Lv = (const int*)(mem + L.o_lv);
@@ -577,9 +577,9 @@ __device__ void trisum_frame(const View& g, int a, char* mem, const FrameLayout&
   auto local_edge = [&](int j, int k, int64_t q) {
     const u64 t_jk = tcs[q] >> kTriShift;
     // edge (x_j, x_k), lo side x_j, third vertex a
-    atomicAdd(&tsl[q], (u64)tL[j]);
-    atomicAdd(&tsh[q], (u64)tL[k]);
-    atomicAdd(&tsd[q], deg_a);
+    atomicAdd(&tsl[q], (ST)tL[j]);
+    atomicAdd(&tsh[q], (ST)tL[k]);
+    atomicAdd(&tsd[q], (ST)deg_a);
     // edge (a, x_j): third vertex x_k; edge (a, x_k): third vertex x_j
     atomicAdd(&acc[3 * j], (AccT)tL[k]);
     atomicAdd(&acc[3 * j + 1], (AccT)t_jk);
@@ -605,23 +605,23 @@ __device__ void trisum_frame(const View& g, int a, char* mem, const FrameLayout&
   __syncthreads();
   for (int j = threadIdx.x; j < D; j += NT) {
     if (acc[3 * j + 2] == 0) continue;  // no triangle on edge (a, x_j)
-    atomicAdd(&tsl[base + j], (u64)acc[3 * j]);
-    atomicAdd(&tsh[base + j], (u64)acc[3 * j + 1]);
-    atomicAdd(&tsd[base + j], (u64)acc[3 * j + 2]);
+    atomicAdd(&tsl[base + j], (ST)acc[3 * j]);
+    atomicAdd(&tsh[base + j], (ST)acc[3 * j + 1]);
+    atomicAdd(&tsd[base + j], (ST)acc[3 * j + 2]);
   }
   __syncthreads();
 }
 
-template <int NT, bool GM, typename AccT>
+template <int NT, bool GM, typename AccT, typename ST>
 __global__ void __launch_bounds__(NT)
 k_trisum_frames(View g, const int* __restrict__ frames, int nframes, int rank, int world,
                 FrameLayout L, char* gslab, const int64_t* __restrict__ OP,
-                const u64* __restrict__ tcs, u64* __restrict__ tsl, u64* __restrict__ tsh,
-                u64* __restrict__ tsd, HitLists HL) {
+                const u64* __restrict__ tcs, ST* __restrict__ tsl, ST* __restrict__ tsh,
+                ST* __restrict__ tsd, HitLists HL) {
   extern __shared__ __align__(16) char smem[];
   char* mem = GM ? gslab + (size_t)blockIdx.x * L.bytes : smem;
   for (int f = rank + world * blockIdx.x; f < nframes; f += world * gridDim.x)
-    trisum_frame<NT, AccT>(g, frames[f], mem, L, OP, tcs, tsl, tsh, tsd, HL);
+    trisum_frame<NT, AccT, ST>(g, frames[f], mem, L, OP, tcs, tsl, tsh, tsd, HL);
 }
 
 // Upper bound of the local-edge count of all frames: sum_a min(items_a, C(D_a, 2)).
@@ -757,10 +757,10 @@ struct HashCounter {  // shared-memory open-addressing hash, u32 or u16 counts
 // alternating with the per-edge atomics.  Steps that cross a row boundary
 // walk their items one at a time.
 // Returns the thread's partial (kUse: sum of cnt-1; kTake: sum of c*(c-1)).
-template <int NT, int MODE, typename C, int U = 1>
+template <int NT, int MODE, typename C, int U = 1, typename CT = u64>
 __device__ __forceinline__ u64 wedge_sweep(const View& g, const int64_t* __restrict__ WP,
                                            int64_t b, int64_t o, int64_t i0, int64_t i1,
-                                           const C& ctr, bool per_edge, u64* __restrict__ c4s) {
+                                           const C& ctr, bool per_edge, CT* __restrict__ c4s) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int nw = NT / 32;
   const int64_t per = (((i1 - i0) + nw - 1) / nw + 31) & ~int64_t(31);
@@ -789,10 +789,10 @@ __device__ __forceinline__ u64 wedge_sweep(const View& g, const int64_t* __restr
         local += c;
         if (per_edge) {
 #ifndef GD_EXP_NO_C4S  // timing experiment only (tools/build_variant.py)
-          atomicAdd(&c4s[q], c);  // edge w-x
+          atomicAdd(&c4s[q], (CT)c);  // edge w-x
 #endif
           if (pr != ptop) {
-            if (top) atomicAdd(&c4s[ptop], top);
+            if (top) atomicAdd(&c4s[ptop], (CT)top);
             top = 0;
             ptop = pr;
           }
@@ -830,15 +830,15 @@ __device__ __forceinline__ u64 wedge_sweep(const View& g, const int64_t* __restr
       }
     }
   }
-  if (MODE == kUse && per_edge && top) atomicAdd(&c4s[ptop], top);
+  if (MODE == kUse && per_edge && top) atomicAdd(&c4s[ptop], (CT)top);
   return local;
 }
 
 // Small and medium frames: counters in a shared-memory hash.
-template <int NT, bool C16>
+template <int NT, bool C16, typename CT>
 __global__ void __launch_bounds__(NT)
 k_c4_frames_smem(View g, const int64_t* __restrict__ WP, const int* __restrict__ frames,
-                 int nframes, int rank, int world, int hcap, int per_edge, u64* __restrict__ c4s,
+                 int nframes, int rank, int world, int hcap, int per_edge, CT* __restrict__ c4s,
                  u64* __restrict__ c4tot2) {
   extern __shared__ __align__(16) char smem[];
   int* hk = (int*)smem;
@@ -856,7 +856,7 @@ k_c4_frames_smem(View g, const int64_t* __restrict__ WP, const int* __restrict__
     for (int h = threadIdx.x; h < H; h += NT) hk[h] = -1;
     for (int h = threadIdx.x; h < (C16 ? H / 2 : H); h += NT) hv[h] = 0u;
     __syncthreads();
-    wedge_sweep<NT, kCount>(g, WP, b, o, i0, i1, ctr, false, c4s);
+    wedge_sweep<NT, kCount, HashCounter<C16>, 1, CT>(g, WP, b, o, i0, i1, ctr, false, c4s);
     __syncthreads();
     u64 local = 0;
     if (!per_edge) {
@@ -865,7 +865,7 @@ k_c4_frames_smem(View g, const int64_t* __restrict__ WP, const int* __restrict__
         local += c * (c - (c > 0));  // 2 * C(c, 2)
       }
     } else {
-      local = wedge_sweep<NT, kUse>(g, WP, b, o, i0, i1, ctr, true, c4s);
+      local = wedge_sweep<NT, kUse, HashCounter<C16>, 1, CT>(g, WP, b, o, i0, i1, ctr, true, c4s);
     }
     const u64 sum = BR(tmp).Sum(local);
     if (threadIdx.x == 0 && sum) atomic_add_u128(c4tot2 + 2 * graph_of(g, s), sum);
@@ -882,11 +882,11 @@ struct HubChunk {
   int64_t i0, i1;  // item range
 };
 
-template <int NT>
+template <int NT, typename CT>
 __global__ void __launch_bounds__(NT)
 k_c4_hub(View g, const int64_t* __restrict__ WP, const HubChunk* __restrict__ chunks,
          unsigned* __restrict__ slabs, int64_t slab_stride, int phase, int per_edge,
-         u64* __restrict__ c4s, u64* __restrict__ c4tot2) {
+         CT* __restrict__ c4s, u64* __restrict__ c4tot2) {
   typedef cub::BlockReduce<u64, NT> BR;
   __shared__ typename BR::TempStorage tmp;
   const HubChunk ch = chunks[blockIdx.x];
@@ -894,13 +894,14 @@ k_c4_hub(View g, const int64_t* __restrict__ WP, const HubChunk* __restrict__ ch
   const int s = ch.frame;
   const int64_t b = g.rp[s], o = g.osplit[s];
   if (phase == 0) {
-    wedge_sweep<NT, kCount>(g, WP, b, o, ch.i0, ch.i1, ctr, false, c4s);
+    wedge_sweep<NT, kCount, SlabCounter, 1, CT>(g, WP, b, o, ch.i0, ch.i1, ctr, false, c4s);
   } else if (phase == 1) {
-    const u64 local = wedge_sweep<NT, kUse>(g, WP, b, o, ch.i0, ch.i1, ctr, per_edge != 0, c4s);
+    const u64 local =
+        wedge_sweep<NT, kUse, SlabCounter, 1, CT>(g, WP, b, o, ch.i0, ch.i1, ctr, per_edge != 0, c4s);
     const u64 sum = BR(tmp).Sum(local);
     if (threadIdx.x == 0 && sum) atomic_add_u128(c4tot2 + 2 * graph_of(g, s), sum);
   } else {
-    wedge_sweep<NT, kZero>(g, WP, b, o, ch.i0, ch.i1, ctr, false, c4s);
+    wedge_sweep<NT, kZero, SlabCounter, 1, CT>(g, WP, b, o, ch.i0, ch.i1, ctr, false, c4s);
   }
 }
 
@@ -928,11 +929,11 @@ struct DsmemCounter {
   __device__ __forceinline__ void zero(int) const {}
 };
 
-template <int NT>
+template <int NT, typename CT>
 __global__ void __launch_bounds__(NT, 1)
 k_c4_cluster(View g, const int64_t* __restrict__ WP, const int* __restrict__ frames,
              int nframes, int rank, int world, int* __restrict__ queue, int per, int per_edge,
-             u64* __restrict__ c4s, u64* __restrict__ c4tot2) {
+             CT* __restrict__ c4s, u64* __restrict__ c4tot2) {
   extern __shared__ __align__(16) unsigned slab[];
   __shared__ int s_frame;
   typedef cub::BlockReduce<u64, NT> BR;
@@ -959,10 +960,12 @@ k_c4_cluster(View g, const int64_t* __restrict__ WP, const int* __restrict__ fra
     const int64_t len = (fi1 - fi0 + csize - 1) / csize;
     const int64_t i0 = fi0 + len * crank;
     const int64_t i1 = i0 + len < fi1 ? i0 + len : fi1;
-    if (i0 < i1) wedge_sweep<NT, kCount>(g, WP, b, o, i0, i1, ctr, false, c4s);
+    if (i0 < i1) wedge_sweep<NT, kCount, DsmemCounter, 1, CT>(g, WP, b, o, i0, i1, ctr, false, c4s);
     cluster.sync();
     const u64 local =
-        i0 < i1 ? wedge_sweep<NT, kUse>(g, WP, b, o, i0, i1, ctr, per_edge != 0, c4s) : 0;
+        i0 < i1 ? wedge_sweep<NT, kUse, DsmemCounter, 1, CT>(g, WP, b, o, i0, i1, ctr, per_edge != 0,
+                                                             c4s)
+                : 0;
     const u64 sum = BR(tmp).Sum(local);
     if (threadIdx.x == 0 && sum) atomic_add_u128(c4tot2 + 2 * graph_of(g, s), sum);
     cluster.sync();  // every remote read of this frame done
@@ -1008,9 +1011,9 @@ struct FlowPlan {
   int nsets;            // slab sets (round r uses set r % nsets)
 };
 
-template <int NT, int MODE, int U>
+template <int NT, int MODE, int U, typename CT>
 __device__ __forceinline__ u64 flow_chunk(const View& g, const int64_t* __restrict__ WP, const FlowPlan& P, int r,
-                          int64_t k, unsigned* __restrict__ set, bool per_edge, u64* __restrict__ c4s,
+                          int64_t k, unsigned* __restrict__ set, bool per_edge, CT* __restrict__ c4s,
                           int& s_out) {
   const int f0 = P.rf[r], f1 = P.rf[r + 1];
   k += P.cpre[f0];
@@ -1028,7 +1031,7 @@ __device__ __forceinline__ u64 flow_chunk(const View& g, const int64_t* __restri
   const int64_t i0 = fi0 + (k - P.cpre[j]) * CH;
   const int64_t i1 = i0 + CH < fi1 ? i0 + CH : fi1;
   U16Counter ctr{set + (size_t)(j - f0) * P.slab_words - (P.x0 >> 1)};
-  return wedge_sweep<NT, MODE, U16Counter, U>(g, WP, b, o, i0, i1, ctr, per_edge, c4s);
+  return wedge_sweep<NT, MODE, U16Counter, U, CT>(g, WP, b, o, i0, i1, ctr, per_edge, c4s);
 }
 
 #ifndef GD_FLOW_MINB
@@ -1040,10 +1043,10 @@ __device__ __forceinline__ u64 flow_chunk(const View& g, const int64_t* __restri
 #ifndef GD_FLOW_UU
 #define GD_FLOW_UU 2
 #endif
-template <int NT, int MINB, int U, int UU>
+template <int NT, int MINB, int U, int UU, typename CT>
 __global__ void __launch_bounds__(NT, MINB)
 k_c4_flow(View g, const int64_t* __restrict__ WP, FlowPlan P, unsigned* __restrict__ slabs,
-          int per_edge, u64* __restrict__ c4s, u64* __restrict__ c4tot2,
+          int per_edge, CT* __restrict__ c4s, u64* __restrict__ c4tot2,
           unsigned long long* __restrict__ next_task, int* __restrict__ done) {
   typedef cub::BlockReduce<u64, NT> BR;
   __shared__ typename BR::TempStorage tmp;
@@ -1076,15 +1079,15 @@ k_c4_flow(View g, const int64_t* __restrict__ WP, FlowPlan P, unsigned* __restri
     unsigned* set = slabs + (size_t)(r % P.nsets) * set_words;
     if (sg.type == kFlowCount) {
       int s;
-      flow_chunk<NT, kCount, U>(g, WP, P, r, k, set, false, c4s, s);
+      flow_chunk<NT, kCount, U, CT>(g, WP, P, r, k, set, false, c4s, s);
     } else if (sg.type == kFlowUse) {
       int s;
-      const u64 local = flow_chunk<NT, kUse, UU>(g, WP, P, r, k, set, per_edge != 0, c4s, s);
+      const u64 local = flow_chunk<NT, kUse, UU, CT>(g, WP, P, r, k, set, per_edge != 0, c4s, s);
       const u64 sum = BR(tmp).Sum(local);
       if (threadIdx.x == 0 && sum) atomic_add_u128(c4tot2 + 2 * graph_of(g, s), sum);
     } else if (sg.type == kFlowZeroSweep) {
       int s;
-      flow_chunk<NT, kZero, U>(g, WP, P, r, k, set, false, c4s, s);
+      flow_chunk<NT, kZero, U, CT>(g, WP, P, r, k, set, false, c4s, s);
     } else {
       // piece k of the round's used slabs: fill with zeros, or (global mode)
       // sum 2*C(c,2) of its counters and zero them
@@ -1153,13 +1156,18 @@ struct EdgeIn {
   const int64_t* e2o;
   const int64_t* e2i;
   const u64* tcs;
-  const u64* tsl;  // null in global mode
-  const u64* tsh;
-  const u64* tsd;
-  const u64* c4s;
+  const void* tsl;  // null in global mode
+  const void* tsh;
+  const void* tsd;
+  const void* c4s;
+  bool narrow;      // per-slot sums held as u32 (max degree < 65536)
   const u64* vT;
   const u64* vS;
 };
+
+__device__ __forceinline__ long long slot_val(const void* p, int64_t q, bool narrow) {
+  return narrow ? (long long)((const unsigned*)p)[q] : (long long)((const u64*)p)[q];
+}
 
 // per-edge contribution to the 13 CensusSums (census.py:449-462)
 __device__ __forceinline__ void add_sums(u128* acc, long long t, long long su, long long sv,
@@ -1195,13 +1203,13 @@ __device__ __forceinline__ void edge_row(const EdgeIn& in, int64_t e, long long*
   row[3] = cl;
   if (!in.tsl) return;
   // out-slot sums are by rank side: lo = lower-rank endpoint
-  const long long slo = (long long)in.tsl[qo], shi = (long long)in.tsh[qo];
+  const long long slo = slot_val(in.tsl, qo, in.narrow), shi = slot_val(in.tsh, qo, in.narrow);
   const long long sumU = ru < rv ? slo : shi, sumV = ru < rv ? shi : slo;
-  const long long tdeg = (long long)in.tsd[qo];
+  const long long tdeg = slot_val(in.tsd, qo, in.narrow);
   const long long tsu = sumU - 2 * cl - t, tsv = sumV - 2 * cl - t, ts = tsu + tsv;
   const long long uu = (long long)in.vT[ru] - t - cl - tsu;
   const long long vv = (long long)in.vT[rv] - t - cl - tsv;
-  const long long c4 = (long long)(in.c4s[qo] + in.c4s[in.e2i[e]]);
+  const long long c4 = slot_val(in.c4s, qo, in.narrow) + slot_val(in.c4s, in.e2i[e], in.narrow);
   const long long cy = c4 - ts - 2 * cl;
   const long long sdeg = (long long)in.vS[ru] - dv + (long long)in.vS[rv] - du - 2 * tdeg;
   const long long ti = tdeg - 2 * t - 2 * cl - ts;
@@ -1528,13 +1536,22 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   WBuf tcs = wz("tcs", S), vT = wz("vT", n), k4tot = wz("k4tot", 2 * G),
        c4tot2 = wz("c4tot2", 2 * G);
   WBuf vS{ws_get<u64>(g, "vS", n, s)};
+  // per-slot pass-B sums and 4-cycle partials: u32 when the maximum degree
+  // is below 2^16 (every partial of slot q is bounded by a quantity of its
+  // edge e = (u, v): C4(e) <= (d(u)-1)(d(v)-1), sum_{w in Tri_e} t(lo, w) and
+  // sum d(w) <= (dmax-1) dmax < 2^32), halving the sectors of their coalesced
+  // atomics; u64 otherwise and for real shards (64-bit NCCL sums)
+  const bool narrow = per_edge && !sh.real() && g.max_deg < 65536 &&
+                      env_int("GD_WIDE_SLOTS", 0) == 0;
+  const size_t slot_words = narrow ? (S + 1) / 2 : S;
   WBuf tsl{nullptr}, tsh{nullptr}, tsd{nullptr}, c4s{nullptr};
   if (per_edge) {
-    tsl = wz("tsl", S);
-    tsh = wz("tsh", S);
-    tsd = wz("tsd", S);
-    c4s = wz("c4s", S);
+    tsl = wz("tsl", slot_words);
+    tsh = wz("tsh", slot_words);
+    tsd = wz("tsd", slot_words);
+    c4s = wz("c4s", slot_words);
   }
+  stat("narrow_slots", narrow ? 1 : 0);
 
   // ---- schedule: item prefixes and frame orders ---------------------------
   struct IBuf { int64_t* p; };
@@ -1659,9 +1676,11 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       set_smem(k_tri_frames<NTV, true, false>, sm);                                          \
       GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tri_frames<NTV, false, false>, NTV, sm)); \
     } else {                                                                                 \
-      set_smem(k_trisum_frames<NTV, false, unsigned>, sm);                                   \
-      set_smem(k_trisum_frames<NTV, false, u64>, sm);                                        \
-      GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trisum_frames<NTV, false, u64>, NTV, sm)); \
+      set_smem(k_trisum_frames<NTV, false, unsigned, u64>, sm);                              \
+      set_smem(k_trisum_frames<NTV, false, u64, u64>, sm);                                   \
+      set_smem(k_trisum_frames<NTV, false, unsigned, unsigned>, sm);                         \
+      set_smem(k_trisum_frames<NTV, false, u64, unsigned>, sm);                              \
+      GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trisum_frames<NTV, false, u64, u64>, NTV, sm)); \
     }                                                                                        \
   }
       switch (bn.nt) {
@@ -1690,6 +1709,21 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
         HL.hcnt = hit_cap ? hcnt : nullptr;
       }
       for (const int rk : my_ranks) {
+#define GD_TRISUM_LAUNCH(NTV, ST)                                                            \
+  {                                                                                          \
+    ST* ql = (ST*)tsl.p;                                                                     \
+    ST* qh = (ST*)tsh.p;                                                                     \
+    ST* qd = (ST*)tsd.p;                                                                     \
+    if (sp)                                                                                  \
+      k_trisum_frames<NTV, true, u64, ST><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, \
+                                                                sp, OP.p, tcs.p, ql, qh, qd, HL); \
+    else if (acc32)                                                                          \
+      k_trisum_frames<NTV, false, unsigned, ST><<<grid, NTV, sm, s>>>(                        \
+          v, fr, (int)nf, rk, world, L, sp, OP.p, tcs.p, ql, qh, qd, HL);                    \
+    else                                                                                     \
+      k_trisum_frames<NTV, false, u64, ST><<<grid, NTV, sm, s>>>(                             \
+          v, fr, (int)nf, rk, world, L, sp, OP.p, tcs.p, ql, qh, qd, HL);                    \
+  }
 #define GD_TRI_LAUNCH(NTV)                                                                   \
   if (!trisum && blocked) {                                                                  \
     if (sp)                                                                                  \
@@ -1708,17 +1742,10 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
                                                             OP.p, tcs.p, vT.p, k4tot.p, HL);  \
     GD_LAUNCH_CHECK("tri_frames");                                                           \
   } else {                                                                                   \
-    if (sp)                                                                                  \
-      k_trisum_frames<NTV, true, u64><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp,  \
-                                                            OP.p, tcs.p, tsl.p, tsh.p, tsd.p, \
-                                                            HL);                               \
-    else if (acc32)                                                                          \
-      k_trisum_frames<NTV, false, unsigned><<<grid, NTV, sm, s>>>(                            \
-          v, fr, (int)nf, rk, world, L, sp, OP.p, tcs.p, tsl.p, tsh.p, tsd.p, HL);           \
+    if (narrow)                                                                              \
+      GD_TRISUM_LAUNCH(NTV, unsigned)                                                        \
     else                                                                                     \
-      k_trisum_frames<NTV, false, u64><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp, \
-                                                             OP.p, tcs.p, tsl.p, tsh.p,      \
-                                                             tsd.p, HL);                     \
+      GD_TRISUM_LAUNCH(NTV, u64)                                                             \
     GD_LAUNCH_CHECK("trisum_frames");                                                        \
   }
       switch (bn.nt) {
@@ -1730,6 +1757,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       }
       }
 #undef GD_TRI_LAUNCH
+#undef GD_TRISUM_LAUNCH
     }
   };
   run_frames(false);
@@ -1818,10 +1846,14 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     if (!f16.empty() && csize) {
       constexpr int NT = 512;
       const size_t sm = (size_t)per * 2;
-      auto kern = k_c4_cluster<NT>;
+      auto kern = k_c4_cluster<NT, u64>;
+      auto kern32 = k_c4_cluster<NT, unsigned>;
       set_smem(kern, sm);
-      if (csize > 8)
+      set_smem(kern32, sm);
+      if (csize > 8) {
         GD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        GD_CUDA(cudaFuncSetAttribute(kern32, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      }
       cudaLaunchConfig_t cfg = {};
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1844,11 +1876,14 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       queue.zero();
       GD_CUDA(cudaMemcpyAsync(dfr.p, f16_all.data(), f16_all.size() * 4, cudaMemcpyHostToDevice,
                               s));
-      const int* WPc = nullptr;
-      (void)WPc;
-      GD_CUDA(cudaLaunchKernelEx(&cfg, kern, v, (const int64_t*)WP.p, (const int*)dfr.p,
-                                 (int)f16_all.size(), rk, world, queue.p, per, pe, c4s_p,
-                                 c4tot2.p));
+      if (narrow)
+        GD_CUDA(cudaLaunchKernelEx(&cfg, kern32, v, (const int64_t*)WP.p, (const int*)dfr.p,
+                                   (int)f16_all.size(), rk, world, queue.p, per, pe,
+                                   (unsigned*)c4s_p, c4tot2.p));
+      else
+        GD_CUDA(cudaLaunchKernelEx(&cfg, kern, v, (const int64_t*)WP.p, (const int*)dfr.p,
+                                   (int)f16_all.size(), rk, world, queue.p, per, pe, c4s_p,
+                                   c4tot2.p));
       GD_LAUNCH_CHECK("c4_cluster");
       nrounds = -csize;  // reported as the cluster size
     } else if (!f16.empty()) {
@@ -1857,7 +1892,8 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       // 4 CTAs/SM (32 registers) and 2 items per lane in flight: measured
       // 72.6 ms vs 87.6 (3 CTAs, 1 item) on config 3; the use sweep's
       // dependent counter reads are latency-bound
-      auto fk = k_c4_flow<NT, GD_FLOW_MINB, GD_FLOW_U, GD_FLOW_UU>;
+      auto fk = k_c4_flow<NT, GD_FLOW_MINB, GD_FLOW_U, GD_FLOW_UU, u64>;
+      auto fk32 = k_c4_flow<NT, GD_FLOW_MINB, GD_FLOW_U, GD_FLOW_UU, unsigned>;
       const int fnt = NT;
       GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fk, fnt, 0));
       if (per_sm < 1) throw Error(GD_ECUDA, "c4 flow kernel cannot be resident");
@@ -1953,7 +1989,11 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       FlowPlan P{dfr.p, dcp.p, drf.p, drch.p, dseg.p, (int)segs.size(), F, slab_words, x0,
                  pieces, NS};
       nrounds += R;
-      fk<<<grid, fnt, 0, s>>>(v, WP.p, P, slabs, pe, c4s_p, c4tot2.p, ntask.p, done.p);
+      if (narrow)
+        fk32<<<grid, fnt, 0, s>>>(v, WP.p, P, slabs, pe, (unsigned*)c4s_p, c4tot2.p, ntask.p,
+                                  done.p);
+      else
+        fk<<<grid, fnt, 0, s>>>(v, WP.p, P, slabs, pe, c4s_p, c4tot2.p, ntask.p, done.p);
       GD_LAUNCH_CHECK("c4_flow");
     }
     timer.mark("c4_coop");
@@ -1988,8 +2028,12 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
         GD_CUDA(cudaMemcpyAsync(dch.p, chunks.data(), chunks.size() * sizeof(HubChunk),
                                 cudaMemcpyHostToDevice, s));
         for (int phase = 0; phase < 3; phase++) {
-          k_c4_hub<512><<<(int)chunks.size(), 512, 0, s>>>(v, WP.p, dch.p, slabs.p, slab_stride,
-                                                           phase, pe, c4s_p, c4tot2.p);
+          if (narrow)
+            k_c4_hub<512, unsigned><<<(int)chunks.size(), 512, 0, s>>>(
+                v, WP.p, dch.p, slabs.p, slab_stride, phase, pe, (unsigned*)c4s_p, c4tot2.p);
+          else
+            k_c4_hub<512, u64><<<(int)chunks.size(), 512, 0, s>>>(
+                v, WP.p, dch.p, slabs.p, slab_stride, phase, pe, c4s_p, c4tot2.p);
           GD_LAUNCH_CHECK("c4_hub");
         }
         GD_CUDA(cudaStreamSynchronize(s));
@@ -1998,7 +2042,8 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     }
     }  // shards
   }
-  auto smem_bin = [&](std::pair<int64_t, int64_t> r, auto kernel, int nt, bool c16, int per_sm) {
+  auto smem_bin = [&](std::pair<int64_t, int64_t> r, auto kernel, auto kernel32, int nt, bool c16,
+                      int per_sm) {
     const int64_t nf = r.second - r.first;
     if (nf <= 0) return;
     // capacity > max distinct counters (<= wedges): load <= 1/2 (u32 bins)
@@ -2009,27 +2054,34 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     const size_t sm = (size_t)hcap * 4 + (size_t)hcap * (c16 ? 2 : 4);
     if (sm > 200 * 1024) throw Error(GD_EINVAL, "wedge frame too large for the shared hash");
     set_smem(kernel, sm);
+    set_smem(kernel32, sm);
     const int grid =
         (int)std::min<int64_t>((nf + world - 1) / world, (int64_t)num_sms() * per_sm);
     for (const int rk : my_ranks) {
-      kernel<<<grid, nt, sm, s>>>(v, WP.p, c4_frames.p + r.first, (int)nf, rk, world, hcap, pe,
-                                  c4s_p, c4tot2.p);
+      if (narrow)
+        kernel32<<<grid, nt, sm, s>>>(v, WP.p, c4_frames.p + r.first, (int)nf, rk, world, hcap,
+                                      pe, (unsigned*)c4s_p, c4tot2.p);
+      else
+        kernel<<<grid, nt, sm, s>>>(v, WP.p, c4_frames.p + r.first, (int)nf, rk, world, hcap, pe,
+                                    c4s_p, c4tot2.p);
       GD_LAUNCH_CHECK("c4_frames_smem");
     }
   };
+#define GD_SMK(NT_, C16_) k_c4_frames_smem<NT_, C16_, u64>, k_c4_frames_smem<NT_, C16_, unsigned>
   // hash capacity grows with the bin's largest frame: finer bins keep more
   // CTAs resident per SM (u16 counts above 4096 wedges)
   if (env_int("GD_C4_TOP_NT", 1024) == 1024)
-    smem_bin(rs2, k_c4_frames_smem<1024, true>, 1024, true, 1);
+    smem_bin(rs2, GD_SMK(1024, true), 1024, true, 1);
   else
-    smem_bin(rs2, k_c4_frames_smem<512, true>, 512, true, 1);
+    smem_bin(rs2, GD_SMK(512, true), 512, true, 1);
   if (env_int("GD_C4_MID_NT", 1024) == 1024)
-    smem_bin(rsb, k_c4_frames_smem<1024, true>, 1024, true, 2);
+    smem_bin(rsb, GD_SMK(1024, true), 1024, true, 2);
   else
-    smem_bin(rsb, k_c4_frames_smem<512, true>, 512, true, 2);
-  smem_bin(rs1, k_c4_frames_smem<256, false>, 256, false, 3);
-  smem_bin(rsa, k_c4_frames_smem<128, false>, 128, false, 12);
-  smem_bin(rs0, k_c4_frames_smem<64, false>, 64, false, 32);
+    smem_bin(rsb, GD_SMK(512, true), 512, true, 2);
+  smem_bin(rs1, GD_SMK(256, false), 256, false, 3);
+  smem_bin(rsa, GD_SMK(128, false), 128, false, 12);
+  smem_bin(rs0, GD_SMK(64, false), 64, false, 32);
+#undef GD_SMK
   timer.mark("c4_smem");
   if (sh.real() && per_edge) {  // per-slot triangle sums and 4-cycle counts of all shards
     sh.allreduce(tsl.p, (size_t)S);
@@ -2054,6 +2106,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   in.e2o = g.e2o.p;
   in.e2i = g.e2i.p;
   in.tcs = tcs.p;
+  in.narrow = narrow;
   in.tsl = per_edge ? tsl.p : nullptr;
   in.tsh = per_edge ? tsh.p : nullptr;
   in.tsd = per_edge ? tsd.p : nullptr;

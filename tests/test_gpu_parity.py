@@ -61,7 +61,7 @@ def test_degenerate_graphs():
 
 
 FORCED = ["tri_gmem", "tri_small", "tri_blocks", "c4_coop", "c4_hub32", "c4_smem",
-          "c4_flow", "tri_gmem,c4_coop", "tri_small,c4_hub32"]
+          "c4_flow", "tri_gmem,c4_coop", "tri_small,c4_hub32", "wide_slots", "c4_flow,wide_slots"]
 
 
 def _dense_cases():
@@ -100,6 +100,8 @@ for name, n, edges in T._dense_cases():
 print("ok")
 ''' % (str(GOLDEN.parent.parent), str(GOLDEN.parent))
     env = dict(os.environ, GD_FORCE_PATH=force)
+    if "wide_slots" in force:  # 64-bit per-slot sums even where 32 bits suffice
+        env["GD_WIDE_SLOTS"] = "1"
     if force == "tri_small,c4_hub32":
         env["GD_HIT_CAP"] = "5000"  # hit-buffer overflow: pass B re-probes some frames
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
@@ -226,6 +228,8 @@ for name, n, edges in T._dense_cases():
 print("ok")
 ''' % (str(GOLDEN.parent.parent), str(GOLDEN.parent))
     env = dict(os.environ, GD_FORCE_PATH=force)
+    if "wide_slots" in force:  # 64-bit per-slot sums even where 32 bits suffice
+        env["GD_WIDE_SLOTS"] = "1"
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
