@@ -406,7 +406,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                          "kernel": "census pipeline (B_alg of SURVEY 8(d) / summed kernel time)",
                          "dominant_phase": dom[0],
                          "dominant_share": dom[1] / max(ms, 1e-9),
-                         "ncu_kernel": ncu_kernel},
+                         "ncu_kernel": ncu_kernel,
+                         # the dominant phase's kernel: ncu DRAM bytes of one
+                         # launch over its live CUDA-event time in this run
+                         "dominant_dram_gbs": (ncu_kernel["dram_bytes"] / (dom[1] / 1e3) / 1e9
+                                               if ncu_kernel and dom[1] > 0 else None)},
             "phases_ms": {k: round(v, 3) for k, v in phases.items()},
             "work": {k: v for k, v in stats.items() if k != "launches"},
             "wall_ms_per_step": wall_ms,
