@@ -207,7 +207,7 @@ __device__ int frame_load(const View& g, int a, char* mem, const FrameLayout& L,
 // U items per lane in flight (their col[] loads are issued back to back).
 // f(j, i, q, y) receives the slot q = QB[j] + i and the neighbour y = col[q].
 #ifndef GD_TRI_K
-#define GD_TRI_K 8
+#define GD_TRI_K 32
 #endif
 #ifndef GD_TRI_U
 #define GD_TRI_U 1
@@ -527,8 +527,13 @@ __device__ void tri_frame(const View& g, int a, char* mem, const FrameLayout& L,
 // GM: frame scratch in a global slab (largest frames); otherwise in shared
 // memory, where keeping the pointer's provenance static lets the compiler
 // emit LDS/STS/ATOMS instead of generic loads.
+#if defined(GD_TRI_FULL_OCC) && GD_TRI_FULL_OCC
+#define GD_TRI_BOUNDS(NT) __launch_bounds__(NT, (NT) >= 64 ? 2048 / (NT) : 32)
+#else
+#define GD_TRI_BOUNDS(NT) __launch_bounds__(NT)
+#endif
 template <int NT, bool BLOCKED, bool GM>
-__global__ void __launch_bounds__(NT)
+__global__ void GD_TRI_BOUNDS(NT)
 k_tri_frames(View g, const int* __restrict__ frames, int nframes, int rank, int world,
              FrameLayout L, char* gslab, const int64_t* __restrict__ OP, u64* __restrict__ tcs,
              u64* __restrict__ vT, u64* __restrict__ k4tot, HitLists HL) {
