@@ -95,6 +95,21 @@ def feature_matrix(graphs, labels=None, config: ParallelConfig | None = None,
         # rounded; the rare counts beyond int64 go through Python ints
         small = (hi == 0) & (lo >= 0)
         fl = lo.astype(np.float64)
+        if not log_scale and not normalize:
+            # plain counts: whole-matrix conversion, per-row work only for
+            # skipped graphs and counts beyond int64
+            ok = status == 0
+            keep = np.nonzero(ok)[0]
+            matrix = fl[keep]
+            wide = ~small[keep].all(axis=1)
+            for r in np.nonzero(wide)[0]:
+                matrix[r] = [float(v) for v in counts_as_ints(counts[keep[r]])]
+            for i in np.nonzero(~ok)[0]:
+                skipped.append((labels[i], "ConsistencyError: " + _STEP_NAMES[int(status[i]) - 1]
+                                + " failed"))
+            kept = [labels[i] for i in keep]
+            return FeatureMatrix(class_ids, kept, matrix.reshape(len(kept), len(class_ids)),
+                                 [per] * len(kept), skipped)
         for i in range(count):
             if status[i]:
                 skipped.append((labels[i], "ConsistencyError: " + _STEP_NAMES[int(status[i]) - 1]
