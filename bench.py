@@ -387,6 +387,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if rank == 0 and args.batch:
         batch = bench_batch(gd, N, L, with_cpu=world == 1 and not args.no_cpu_baseline)
 
+    big = None
+    if rank == 0 and world == 1 and args.big and args.config == "c3_rmat20":
+        big = bench_resident_config(gd, N, L, "c5_chung_lu_4m", peak)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": m / (ms / 1e3), "unit": "edges/s",
@@ -423,6 +427,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "cpu_baseline": cpu,
             "global_mode": glob,
             "batch_c4": batch,
+            "c5_chung_lu_4m": big,
             "counts": {"g3_1": str(f_ref.counts["g3_1"]), "g4_1": str(f_ref.counts["g4_1"]),
                        "g4_4": str(f_ref.counts["g4_4"])},
         }
@@ -433,6 +438,52 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         comm.close()
     dist.close()
     return 0
+
+
+def bench_resident_config(gd, N, L, config: str, peak: float, steps: int = 3,
+                          warmup: int = 3) -> dict:
+    """A second BASELINE config measured resident (CSR on the device, L2
+    flushed between steps, CUDA events over the whole census): per-edge and
+    global census times, edges/s and SURVEY 8(d) roofline fraction.  Used for
+    config 5 (the north star's 4M-vertex Chung-Lu run) beside config 3."""
+    raw = load_graph(config)
+    g = gd.Graph.from_edges(raw.pairs, gd.ParseOptions(num_vertices=raw.n))
+    del raw
+    n, m = g.n, g.m
+    deg = np.asarray(g.degrees, dtype=np.int64)
+    sum_d2 = int(np.dot(deg, deg))
+    dtab = L.gd_device_alloc(m * 10 * 8)
+    out = {"workload": config, "graph": CONFIG_DESC[config], "n": n, "m": m,
+           "steps": steps, "warmup": warmup,
+           "l2": "flushed between steps", "timing": "CUDA events, whole census"}
+    try:
+        for mode in ("per_edge", "global"):
+            ms, ref = [], None
+            for i in range(warmup + steps):
+                L.gd_flush_l2()
+                if mode == "per_edge":
+                    _, f = gd.micro_census_table(g, device_out=dtab)
+                else:
+                    f = gd.graphlet_census(g)
+                if ref is None:
+                    ref = f
+                elif f != ref:
+                    raise SystemExit(f"{config} {mode}: census result changed between steps")
+                if i >= warmup:
+                    ms.append(sum(gd.last_timings(g).values()))
+            t = statistics.mean(ms)
+            b_alg = m * (8 + 4 * 8 + 8 * (10 if mode == "per_edge" else 0)) + 4 * sum_d2
+            out[mode] = {"ms_per_step": t, "value": m / (t / 1e3), "unit": "edges/s",
+                         "roofline_frac": b_alg / (t / 1e3) / 1e9 / peak,
+                         "algorithmic_bytes": b_alg,
+                         "phases_ms": {k: round(v, 3) for k, v in gd.last_timings(g).items()}}
+        if out["per_edge"] and ref is not None:
+            out["g4_4"] = str(ref.counts["g4_4"])
+    finally:
+        L.gd_device_free(dtab)
+        del g
+        gd.trim_workspace()
+    return out
 
 
 def bench_batch(gd, N, L, with_cpu: bool) -> dict:
@@ -484,6 +535,8 @@ def main():
     ap.add_argument("--no-global", dest="global_too", action="store_false")
     ap.add_argument("--no-batch", dest="batch", action="store_false",
                     help="skip the config-4 batch (feature_matrix) measurement")
+    ap.add_argument("--no-big", dest="big", action="store_false",
+                    help="skip the resident config-5 (Chung-Lu 4M) secondary measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
