@@ -697,9 +697,21 @@ __device__ __forceinline__ int64_t wedge_slot(const int64_t* __restrict__ WP, in
 
 enum WedgeMode { kCount = 0, kUse = 1, kZero = 2, kTake = 3 };
 
+// Fire-and-forget global reductions as PTX `red`.  Written as atomicAdd, a
+// reduction whose result is unused becomes REDG, except in kernels that also
+// hold a fence (the flow kernel's release of a finished task): there ptxas
+// keeps every one of them an ATOMG that tracks its response.  `red` carries
+// the PTX memory-model semantics the fence + barrier protocol relies on.
+__device__ __forceinline__ void red_add(unsigned* a, unsigned v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_add(unsigned long long* a, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+
 struct SlabCounter {  // dense u32 counters in global memory
   unsigned* cnt;
-  __device__ __forceinline__ void inc(int x) const { atomicAdd(&cnt[x], 1u); }
+  __device__ __forceinline__ void inc(int x) const { red_add(&cnt[x], 1u); }
   __device__ __forceinline__ unsigned get(int x) const { return cnt[x]; }
   __device__ __forceinline__ unsigned take(int x) const { return atomicExch(&cnt[x], 0u); }
   __device__ __forceinline__ void zero(int x) const { cnt[x] = 0u; }
@@ -708,7 +720,7 @@ struct SlabCounter {  // dense u32 counters in global memory
 struct U16Counter {  // dense u16 counters, two per 32-bit word
   unsigned* w;
   __device__ __forceinline__ void inc(int x) const {
-    atomicAdd(&w[x >> 1], 1u << ((x & 1) << 4));
+    red_add(&w[x >> 1], 1u << ((x & 1) << 4));
   }
   __device__ __forceinline__ unsigned get(int x) const {
 #ifdef GD_CNT_CG  // experiment: counter reads bypass L1
@@ -794,10 +806,10 @@ __device__ __forceinline__ u64 wedge_sweep(const View& g, const int64_t* __restr
         local += c;
         if (per_edge) {
 #ifndef GD_EXP_NO_C4S  // timing experiment only (tools/build_variant.py)
-          atomicAdd(&c4s[q], (CT)c);  // edge w-x
+          red_add(&c4s[q], (CT)c);  // edge w-x
 #endif
           if (pr != ptop) {
-            if (top) atomicAdd(&c4s[ptop], (CT)top);
+            if (top) red_add(&c4s[ptop], (CT)top);
             top = 0;
             ptop = pr;
           }
@@ -835,7 +847,7 @@ __device__ __forceinline__ u64 wedge_sweep(const View& g, const int64_t* __restr
       }
     }
   }
-  if (MODE == kUse && per_edge && top) atomicAdd(&c4s[ptop], (CT)top);
+  if (MODE == kUse && per_edge && top) red_add(&c4s[ptop], (CT)top);
   return local;
 }
 
