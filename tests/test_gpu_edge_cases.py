@@ -89,3 +89,38 @@ def test_concurrent_censuses_from_threads():
         for i, f, tab, fg in ex.map(run, jobs):
             assert f == want[i][0] and fg == want[i][0]
             assert np.array_equal(tab, want[i][1])
+
+
+def test_nccl_sharded_path_single_rank():
+    """The real-communicator path of the frame-sharded census (NCCL loaded
+    with dlopen, communicator from a torch.distributed group, all-reduce of
+    the 64-bit slot partials, all-gather of the totals) at world size 1 in a
+    subprocess: identical table and counts to the single-GPU census."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, %r)
+import torch.distributed as dist
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:29533", rank=0, world_size=1)
+import paper_1506_04322_b200 as gd
+from paper_1506_04322_b200 import workloads as W
+from paper_1506_04322_b200.distributed import CensusComm, micro_census_table_sharded, graphlet_census_sharded
+raw = W.chung_lu(30_000, 2.1, 8.0, 1500.0, seed=9)
+g = gd.Graph.from_edges(raw.pairs, gd.ParseOptions(num_vertices=raw.n))
+tab0, f0 = gd.micro_census_table(g)
+comm = CensusComm()
+tab1, f1 = micro_census_table_sharded(g, comm)
+f2 = graphlet_census_sharded(g, comm)
+assert f1 == f0 and f2 == f0, (f0, f1, f2)
+assert np.array_equal(np.asarray(tab1), np.asarray(tab0))
+comm.close()
+dist.destroy_process_group()
+print("ok")
+''' % str(root)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, MASTER_ADDR="127.0.0.1"))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
