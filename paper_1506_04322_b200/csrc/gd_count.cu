@@ -1928,7 +1928,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
         x0 &= ~1;
       }
       const int64_t slab_words = ((((int64_t)n - x0) + 1) / 2 + 31) & ~int64_t(31);
-      const int64_t l2_budget = env_int("GD_C4_FLOW_MB", 480) << 20;  // all slab sets
+      const int64_t l2_budget = env_int("GD_C4_FLOW_MB", 640) << 20;  // all slab sets
       // a round's use (or scan) tasks are handed out LU steps after its count
       // tasks and its zeroing one step later; a count task waits for the
       // zeroing of the set it reuses, NS rounds back
