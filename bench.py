@@ -22,6 +22,7 @@ workload; it is the only other place this script executes oracle/.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -353,12 +354,17 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         dev = sum(gd.last_timings(g2).values()) if DEBUG else 0.0
         del g2
         dt = (time.perf_counter() - t0) * 1e3
-        if DEBUG:
-            import torch
-            free_b, tot_b = torch.cuda.mem_get_info()
+        if DEBUG:  # NVML (no CUDA context of its own) for the device memory in use
+            import pynvml
+            pynvml.nvmlInit()
+            used = pynvml.nvmlDeviceGetMemoryInfo(pynvml.nvmlDeviceGetHandleByIndex(local_rank)).used
+            ps = (ctypes.c_uint64 * 4)()
+            L.gd_pool_stats(ps)
             print(f"e2e step {i}: build {1e3 * (tb - t0):.1f} census {1e3 * (tc - tb):.1f} "
                   f"(device {dev:.1f}) free {1e3 * (time.perf_counter() - tc):.1f} "
-                  f"gpu used {(tot_b - free_b) / 2**30:.2f} GiB", file=sys.stderr, flush=True)
+                  f"gpu used {used / 2**30:.2f} GiB pool reserved {ps[0] / 2**30:.2f} "
+                  f"(high {ps[1] / 2**30:.2f}) used {ps[2] / 2**30:.2f} "
+                  f"(high {ps[3] / 2**30:.2f}) GiB", file=sys.stderr, flush=True)
         if i >= e2e_warm:
             e2e_ms.append(dt)
         if f2 != f_ref:

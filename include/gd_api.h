@@ -284,6 +284,11 @@ GD_API int gd_flush_l2(void);
  * (the reference allocates per call, census.py:190-303). */
 GD_API int gd_trim_workspace(void);
 
+/* (new) Diagnostics of the stream-ordered device pool the library allocates
+ * from: out[0] reserved bytes, out[1] reserved high-water mark, out[2] used
+ * bytes, out[3] used high-water mark. */
+GD_API int gd_pool_stats(uint64_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -71,6 +71,7 @@ SIGNATURES = (
     ("gd_host_free", None, [_vp]),
     ("gd_flush_l2", ctypes.c_int, []),
     ("gd_trim_workspace", ctypes.c_int, []),
+    ("gd_pool_stats", ctypes.c_int, [ctypes.POINTER(ctypes.c_uint64)]),
     ("gd_parse_edge_list", ctypes.c_int, [_vp, ctypes.c_int64,
                                           ctypes.POINTER(ctypes.c_char_p), ctypes.c_int,
                                           ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),

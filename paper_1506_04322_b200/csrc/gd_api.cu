@@ -3,7 +3,10 @@
 #include <nccl.h>
 
 #include <cstring>
+#include <cstdlib>
+#include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "gd_build.cuh"
 #include "gd_count.cuh"
@@ -99,13 +102,73 @@ static void init_pool_once() {
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
       uint64_t thr = UINT64_MAX;  // keep freed blocks cached across calls
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+
     }
   });
+}
+
+// Headroom in the stream-ordered pool.  The census workspace stays allocated
+// between calls, so with the pool reserved only up to its high-water mark the
+// transient buffers of the next graph build and census (sort temporaries,
+// the device table) must fit in the few GB left beside it; measured: the
+// build of a fresh R-MAT-20 graph then stalls for 150-480 ms in every few
+// calls, and never once the pool holds spare reserve.  After a census the
+// pool is grown (once per new high-water mark) to used_high + min(used_high
+// / 2, 16 GiB); gd_trim_workspace() gives everything back.
+static void ensure_pool_headroom(cudaStream_t s) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+  uint64_t used_high = 0, reserved = 0;
+  cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &used_high);
+  cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+  const uint64_t target = used_high + std::min<uint64_t>(used_high / 2, 16ull << 30);
+  if (reserved >= target) return;
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, target - reserved, s) == cudaSuccess) {
+    cudaFreeAsync(p, s);
+    cudaStreamSynchronize(s);
+  } else {
+    cudaGetLastError();  // not enough free memory for the headroom: run without it
+  }
+  // the padding allocation is not real use: reset the high-water mark (to
+  // the current use) so the next target follows the censuses, not this padding
+  uint64_t zero = 0;
+  if (cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &zero) != cudaSuccess)
+    cudaGetLastError();
 }
 
 std::map<std::string, WsBuf>& thread_workspace() {
   static thread_local std::map<std::string, WsBuf> w;
   return w;
+}
+
+// Graph streams are recycled through a small process-wide pool instead of
+// being created and destroyed with every graph (a fresh graph per call is the
+// common service pattern; stream creation / destruction is driver work on the
+// host path of every call).
+static std::mutex g_stream_mu;
+static std::vector<cudaStream_t> g_stream_pool;
+
+static cudaStream_t acquire_stream() {
+  {
+    std::lock_guard<std::mutex> lock(g_stream_mu);
+    if (!g_stream_pool.empty()) {
+      cudaStream_t s = g_stream_pool.back();
+      g_stream_pool.pop_back();
+      return s;
+    }
+  }
+  cudaStream_t s = nullptr;
+  GD_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  return s;
+}
+
+static void release_stream(cudaStream_t s) {  // s is idle (synchronized)
+  std::lock_guard<std::mutex> lock(g_stream_mu);
+  if (g_stream_pool.size() < 64) g_stream_pool.push_back(s);
+  else cudaStreamDestroy(s);
 }
 
 static cudaStream_t thread_stream() {
@@ -204,6 +267,7 @@ static void census(gd_graph* h, bool per_edge, int64_t* table, int flags, uint64
                             s));
   GD_CUDA(cudaStreamSynchronize(s));
   store_timings(h, ex);
+  ensure_pool_headroom(s);
   close_cycles(hs.data(), ex, G, per_edge);
   if (sums) std::memcpy(sums, hs.data(), hs.size() * 8);
   if (seen) std::memcpy(seen, hseen.data(), G * 8);
@@ -237,7 +301,7 @@ int gd_graph_create(const int64_t* pairs, int64_t k, int64_t n, int ids_mode, in
   }
   gd_graph* h = new gd_graph();
   int rc = guarded([&] {
-    GD_CUDA(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+    h->s = acquire_stream();
     build_graph(h->g, pairs, k, n, ids_mode, flags, h->s);
   });
   if (rc != GD_OK) {
@@ -258,7 +322,7 @@ int gd_graph_create_batch(const int64_t* pairs, const int64_t* pair_offsets,
   *out = nullptr;
   gd_graph* h = new gd_graph();
   int rc = guarded([&] {
-    GD_CUDA(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+    h->s = acquire_stream();
     build_graph_batch(h->g, pairs, pair_offsets, n_per_graph, num_graphs, flags, h->s);
   });
   if (rc != GD_OK) {
@@ -313,7 +377,7 @@ void gd_graph_free(gd_graph* h) {
   }
   if (h->s) {
     cudaStreamSynchronize(h->s);
-    cudaStreamDestroy(h->s);
+    release_stream(h->s);
   }
   delete h;
 }
@@ -760,6 +824,29 @@ int gd_trim_workspace(void) {
     GD_CUDA(cudaStreamSynchronize(s));
     GD_CUDA(cudaDeviceSynchronize());
     thread_workspace().clear();
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+      cudaMemPoolTrimTo(pool, 0);  // and the pool's spare reserve
+  });
+}
+
+// Device memory pool of the library's allocations: [0] reserved bytes,
+// [1] reserved high-water mark, [2] used bytes, [3] used high-water mark.
+int gd_pool_stats(uint64_t* out) {
+  if (!out) {
+    t_last_error = "out is NULL";
+    return GD_EINVAL;
+  }
+  return guarded([&] {
+    int dev = 0;
+    GD_CUDA(cudaGetDevice(&dev));
+    cudaMemPool_t pool;
+    GD_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    const cudaMemPoolAttr attrs[4] = {cudaMemPoolAttrReservedMemCurrent,
+                                      cudaMemPoolAttrReservedMemHigh,
+                                      cudaMemPoolAttrUsedMemCurrent, cudaMemPoolAttrUsedMemHigh};
+    for (int i = 0; i < 4; i++) GD_CUDA(cudaMemPoolGetAttribute(pool, attrs[i], &out[i]));
   });
 }
 
