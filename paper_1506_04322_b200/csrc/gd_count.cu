@@ -774,18 +774,27 @@ struct HashCounter {  // shared-memory open-addressing hash, u32 or u16 counts
 // alternating with the per-edge atomics.  Steps that cross a row boundary
 // walk their items one at a time.
 // Returns the thread's partial (kUse: sum of cnt-1; kTake: sum of c*(c-1)).
-template <int NT, int MODE, typename C, int U = 1, typename CT = u64>
+template <int NT, int MODE, typename C, int U = 1, typename CT = u64, int PIECES = 1>
 __device__ __forceinline__ u64 wedge_sweep(const View& g, const int64_t* __restrict__ WP,
                                            int64_t b, int64_t o, int64_t i0, int64_t i1,
-                                           const C& ctr, bool per_edge, CT* __restrict__ c4s) {
+                                           const C& ctr, bool per_edge, CT* __restrict__ c4s,
+                                           int* piece_ctr = nullptr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int nw = NT / 32;
-  const int64_t per = (((i1 - i0) + nw - 1) / nw + 31) & ~int64_t(31);
-  const int64_t c0 = i0 + (int64_t)warp * per;
+  // PIECES > 1: nw * PIECES pieces claimed dynamically from a CTA counter
+  const int npieces = nw * PIECES;
+  const int64_t per = (((i1 - i0) + npieces - 1) / npieces + 31) & ~int64_t(31);
+  auto claim = [&]() {
+    int v = 0;
+    if (lane == 0) v = atomicAdd(piece_ctr, 1);
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
+  u64 local = 0;
+  for (int pc = PIECES == 1 ? warp : claim(); pc < npieces; pc = PIECES == 1 ? npieces : claim()) {
+  const int64_t c0 = i0 + (int64_t)pc * per;
   const int64_t c1 = c0 + per < i1 ? c0 + per : i1;
   int64_t i = c0 + lane;
-  u64 local = 0;
-  if (i >= c1) return 0;
+  if (i >= c1) continue;
   int64_t p = wedge_slot(WP, b, o, i);
   int64_t wp1 = WP[p + 1];
   int64_t base = g.rp[g.col[p]] - WP[p];  // slot of item i in row w: base + i
@@ -848,6 +857,7 @@ __device__ __forceinline__ u64 wedge_sweep(const View& g, const int64_t* __restr
     }
   }
   if (MODE == kUse && per_edge && top) red_add(&c4s[ptop], (CT)top);
+  }
   return local;
 }
 
@@ -1028,10 +1038,13 @@ struct FlowPlan {
   int nsets;            // slab sets (round r uses set r % nsets)
 };
 
+#ifndef GD_FLOW_PIECES
+#define GD_FLOW_PIECES 2
+#endif
 template <int NT, int MODE, int U, typename CT>
 __device__ __forceinline__ u64 flow_chunk(const View& g, const int64_t* __restrict__ WP, const FlowPlan& P, int r,
                           int64_t k, unsigned* __restrict__ set, bool per_edge, CT* __restrict__ c4s,
-                          int& s_out) {
+                          int& s_out, int* piece_ctr) {
   const int f0 = P.rf[r], f1 = P.rf[r + 1];
   k += P.cpre[f0];
   int lo = f0, hi = f1;  // frame of chunk k: last j with cpre[j] <= k
@@ -1048,7 +1061,12 @@ __device__ __forceinline__ u64 flow_chunk(const View& g, const int64_t* __restri
   const int64_t i0 = fi0 + (k - P.cpre[j]) * CH;
   const int64_t i1 = i0 + CH < fi1 ? i0 + CH : fi1;
   U16Counter ctr{set + (size_t)(j - f0) * P.slab_words - (P.x0 >> 1)};
-  return wedge_sweep<NT, MODE, U16Counter, U, CT>(g, WP, b, o, i0, i1, ctr, per_edge, c4s);
+  // count sweeps claim pieces dynamically (their warps finish unevenly);
+  // use sweeps keep one contiguous piece per warp (a piece boundary costs a
+  // slot search and a pending per-edge flush)
+  constexpr int PC = MODE == kCount ? GD_FLOW_PIECES : 1;
+  return wedge_sweep<NT, MODE, U16Counter, U, CT, PC>(g, WP, b, o, i0, i1, ctr, per_edge, c4s,
+                                                      piece_ctr);
 }
 
 #ifndef GD_FLOW_MINB
@@ -1068,6 +1086,7 @@ k_c4_flow(View g, const int64_t* __restrict__ WP, FlowPlan P, unsigned* __restri
   typedef cub::BlockReduce<u64, NT> BR;
   __shared__ typename BR::TempStorage tmp;
   __shared__ long long s_task;
+  __shared__ int s_piece;  // dynamic piece counter of the current task
   const int64_t total = P.segs[P.nseg - 1].task0 + P.segs[P.nseg - 1].ntasks;
   const size_t set_words = (size_t)P.F * P.slab_words;
   if (threadIdx.x == 0) s_task = (long long)atomicAdd(next_task, 1ull);
@@ -1085,6 +1104,7 @@ k_c4_flow(View g, const int64_t* __restrict__ WP, FlowPlan P, unsigned* __restri
       if (P.segs[mid].task0 <= task) lo = mid; else hi = mid;
     }
     const FlowSeg sg = P.segs[lo];
+    if (threadIdx.x == 0) s_piece = 0;  // published by the barrier below
     if (threadIdx.x == 0 && sg.dep >= 0) {
       const int need = (int)P.segs[sg.dep].ntasks;
       while (*(volatile int*)&done[sg.dep] < need) __nanosleep(128);
@@ -1096,15 +1116,16 @@ k_c4_flow(View g, const int64_t* __restrict__ WP, FlowPlan P, unsigned* __restri
     unsigned* set = slabs + (size_t)(r % P.nsets) * set_words;
     if (sg.type == kFlowCount) {
       int s;
-      flow_chunk<NT, kCount, U, CT>(g, WP, P, r, k, set, false, c4s, s);
+      flow_chunk<NT, kCount, U, CT>(g, WP, P, r, k, set, false, c4s, s, &s_piece);
     } else if (sg.type == kFlowUse) {
       int s;
-      const u64 local = flow_chunk<NT, kUse, UU, CT>(g, WP, P, r, k, set, per_edge != 0, c4s, s);
+      const u64 local =
+          flow_chunk<NT, kUse, UU, CT>(g, WP, P, r, k, set, per_edge != 0, c4s, s, &s_piece);
       const u64 sum = BR(tmp).Sum(local);
       if (threadIdx.x == 0 && sum) atomic_add_u128(c4tot2 + 2 * graph_of(g, s), sum);
     } else if (sg.type == kFlowZeroSweep) {
       int s;
-      flow_chunk<NT, kZero, U, CT>(g, WP, P, r, k, set, false, c4s, s);
+      flow_chunk<NT, kZero, U, CT>(g, WP, P, r, k, set, false, c4s, s, &s_piece);
     } else {
       // piece k of the round's used slabs: fill with zeros, or (global mode)
       // sum 2*C(c,2) of its counters and zero them
