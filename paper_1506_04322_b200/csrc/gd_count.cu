@@ -1073,7 +1073,7 @@ __device__ __forceinline__ u64 flow_chunk(const View& g, const int64_t* __restri
 #define GD_FLOW_MINB 4
 #endif
 #ifndef GD_FLOW_U
-#define GD_FLOW_U 2
+#define GD_FLOW_U 1
 #endif
 #ifndef GD_FLOW_UU
 #define GD_FLOW_UU 2
