@@ -28,7 +28,9 @@
 // the row of its lower-rank endpoint, e2o); pass C writes either slot and the
 // finalize adds both (e2o + e2i).
 #include <algorithm>
+#include <climits>
 #include <functional>
+#include <type_traits>
 #include <map>
 #include <mutex>
 
@@ -1163,6 +1165,251 @@ k_c4_flow(View g, const int64_t* __restrict__ WP, FlowPlan P, unsigned* __restri
   }
 }
 
+// ------------------------------------------------------------------------
+// Heavy frames on x-tiles in shared memory.  The dense u16 counter array of
+// frame s over ranks [x0, s) is cut into tiles of T counters; job (s, p)
+// counts, on one CTA, only the wedges s-w-x with x in tile p, whose items are
+// the sub-range [TS[w][p], TS[w][p+1]) of every lower row w (TS: per-row tile
+// split slots, k_tile_splits).  Both sweeps then run on shared-memory atomics
+// and loads (measured on B200: >= 1.5 T random u16 atomics/s in shared
+// memory against 0.19 T/s as L2-resident and 0.03 T/s as DRAM-resident global
+// reductions), and no counter ever reaches L2 or HBM.  Per job the CTA's
+// warps claim batches of 32 consecutive lower slots q_s of row s (segments
+// (w, [a, b))), prefix their lengths with a warp scan and walk the items
+// lane-interleaved (consecutive lanes read consecutive slots of one row w).
+// ------------------------------------------------------------------------
+struct TilePlan {
+  const int* frames;    // heavy frames (rank ids), descending wedges
+  const int64_t* jpre;  // [nf+1] job prefix: frame j owns jobs [jpre[j], jpre[j+1])
+  const int* jframe;    // [njobs] frame of each job
+  int nf;
+  int64_t njobs;
+  int x0;               // first counter rank (even)
+  int T;                // counters per tile (multiple of 8)
+  int P1;               // split entries per row (tiles of [x0, n) + 1)
+  const int64_t* TS;    // [n][P1] absolute slot of the first entry >= x0 + p*T
+};
+
+// TS[w][p] = rp[w] + #(entries of row w with rank < x0 + p*T), warp per row:
+// lane j marks the tiles that start at entry j (tile(x_{j-1}) < p <= tile(x_j)).
+__global__ void k_tile_splits(View g, int x0, int T, int P1, int64_t* __restrict__ TS) {
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int lane = lane_id();
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < g.n; w += warps) {
+    const int64_t b = g.rp[w], e = g.rp[w + 1];
+    int64_t* ts = TS + w * P1;
+    int last = -1;  // tile of the last entry seen (all lanes)
+    for (int64_t c = b; c < e; c += 32) {
+      const int64_t q = c + lane;
+      const int t = q < e ? (g.col[q] - x0) / T : INT_MAX;
+      int prev = __shfl_up_sync(0xffffffffu, t, 1);
+      if (lane == 0) prev = last;
+      if (q < e)
+        for (int p = prev + 1; p <= t && p < P1; p++) ts[p] = q;
+      last = __shfl_sync(0xffffffffu, t, 31);
+      if (last == INT_MAX) {  // the row ended inside this chunk: its last tile
+        const unsigned valid = __ballot_sync(0xffffffffu, q < e);
+        last = __shfl_sync(0xffffffffu, t, 31 - __clz(valid));
+      }
+    }
+    for (int p = last + 1 + lane; p < P1; p += 32) ts[p] = e;
+  }
+}
+
+// Items of one chunk of a job's nonempty segments (k: items seg_pre[k] ..
+// seg_pre[k+1] at slots seg_off[k] + item), walked by a warp over the item
+// range [r0, r1) in steps of 32 consecutive items.  The segments after the
+// current one start at distinct items (empty segments are compacted away),
+// so at most 32 of them start inside a step: lane l tests segment kc+1+l, a
+// warp OR collects the start bits M, and lane j's segment is
+// kc + popc(M & bits <= j) -- no search, one shared load per lane.  U steps
+// are resolved before their col[] loads are issued.  f(k, q, x, M, j) gets
+// the segment k (-1 past r1), slot q, x = col[q] and the step's start bits.
+#ifndef GD_TILE_U
+#define GD_TILE_U 2
+#endif
+template <int U, typename F>
+__device__ __forceinline__ void tile_range_items(const View& g, const int* seg_pre,
+                                                 const long long* seg_off, int cnt,
+                                                 int r0, int r1, F&& f) {
+  const int lane = threadIdx.x & 31;
+  const unsigned le = 0xffffffffu >> (31 - lane);  // bits 0..lane
+  // current segment: last k with seg_pre[k] <= r0
+  int lo = 0, hi = cnt;
+  while (lo < hi - 1) {
+    const int mid = (lo + hi) >> 1;
+    if (seg_pre[mid] <= r0) lo = mid; else hi = mid;
+  }
+  int kc = lo;
+  for (int base = r0; base < r1; base += 32 * U) {
+    int kk[U];
+    int64_t qq[U];
+    unsigned mm[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int wb = base + 32 * u;
+      const int k = kc + 1 + lane;
+      const int r = (k < cnt ? seg_pre[k] : INT_MAX) - wb;
+      const unsigned M = __reduce_or_sync(0xffffffffu, r < 32 ? 1u << r : 0u);
+      const int ks = kc + __popc(M & le);
+      kc += __popc(M);
+      kk[u] = wb + lane < r1 ? ks : -1;
+      qq[u] = seg_off[ks] + wb + lane;
+      mm[u] = M;
+    }
+    int xx[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) xx[u] = kk[u] >= 0 ? __ldg(g.col + qq[u]) : 0;
+#pragma unroll
+    for (int u = 0; u < U; u++) f(kk[u], qq[u], xx[u], mm[u]);
+  }
+}
+
+template <int NT, typename CT>
+__global__ void __launch_bounds__(NT, 1)
+k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
+           CT* __restrict__ c4s, u64* __restrict__ c4tot2,
+           unsigned long long* __restrict__ next_job) {
+  constexpr int NW = NT / 32;
+  constexpr int U = GD_TILE_U;
+  constexpr int C = NT;  // segments per chunk (one per thread)
+  // per-edge segment sums: below degree 2^16 a segment's sum is < dmax^2 < 2^32
+  typedef typename std::conditional<std::is_same<CT, unsigned>::value, unsigned, u64>::type SumT;
+  extern __shared__ __align__(16) unsigned tile[];  // T u16 counters
+  __shared__ long long s_job, s_next;
+  __shared__ int s_range;
+  __shared__ long long seg_off[C];
+  __shared__ int seg_pre[C + 1];
+  __shared__ SumT seg_sum[C];
+  __shared__ int seg_slot[C];
+  typedef cub::BlockScan<long long, NT> BS;
+  typedef cub::BlockReduce<u64, NT> BR;
+  __shared__ union {
+    typename BS::TempStorage scan;
+    typename BR::TempStorage red;
+  } tmp;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned short* tile16 = (const unsigned short*)tile;
+  if (threadIdx.x == 0) s_next = (long long)atomicAdd(next_job, 1ull);
+  while (true) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_job = s_next;
+    __syncthreads();
+    const int64_t job = s_job;
+    if (job >= P.njobs) break;
+    // the next job is claimed now: its latency overlaps this one
+    if (threadIdx.x == 0) s_next = (long long)atomicAdd(next_job, 1ull);
+    const int fj = P.jframe[job];
+    const int s = P.frames[fj];
+    const int p = (int)(job - P.jpre[fj]);
+    const bool last = job + 1 == P.jpre[fj + 1];  // tile holding rank s - 1: items capped at s
+    const int X = P.x0 + p * P.T;
+    const int64_t b = g.rp[s], nseg = g.osplit[s] - b;
+    uint4* t4 = (uint4*)tile;
+    for (int i = threadIdx.x; i < P.T / 8; i += NT) t4[i] = make_uint4(0u, 0u, 0u, 0u);
+    u64 local = 0;
+    for (int sweep = 0; sweep < (per_edge ? 2 : 1); sweep++) {
+      for (int64_t c0 = 0; c0 < nseg; c0 += C) {
+        // chunk setup: segment of thread t = lower slot q_s = b + c0 + t
+        const int cnt = (int)(nseg - c0 < C ? nseg - c0 : C);
+        const int64_t qs = b + c0 + threadIdx.x;
+        int64_t a = 0, e = 0;
+        if (threadIdx.x < cnt) {
+          const int w = __ldg(g.col + qs);
+          const int64_t* ts = P.TS + (int64_t)w * P.P1 + p;
+          a = ts[0];
+          e = ts[1];
+          if (last) e = min(e, P.TS[(int64_t)w * P.P1] + (WP[qs + 1] - WP[qs]));
+        }
+        const int len = e > a ? (int)(e - a) : 0;
+        // exclusive prefix of (nonempty flag, length) in one scan: nonempty
+        // segments get dense indices (a step of 32 items then meets at most
+        // 32 segment starts)
+        long long pk, tot;
+        BS(tmp.scan).ExclusiveSum(((long long)(len > 0) << 32) | len, pk, tot);
+        const int pre = (int)(pk & 0xffffffffll), ci = (int)(pk >> 32);
+        const int total = (int)(tot & 0xffffffffll), ncomp = (int)(tot >> 32);
+        if (len > 0) {
+          seg_off[ci] = a - pre;
+          seg_pre[ci] = pre;
+          seg_slot[ci] = (int)(c0 + threadIdx.x);
+        }
+        if (threadIdx.x == 0) {
+          seg_pre[ncomp] = total;
+          s_range = 0;
+        }
+        if (sweep) seg_sum[threadIdx.x] = 0;
+        __syncthreads();
+        // item ranges claimed dynamically: long segments spread over warps
+        const int R = min(1024, max(64, ((total / (4 * NW)) + 31) & ~31));
+        while (true) {
+          int r0 = 0;
+          if (lane == 0) r0 = atomicAdd(&s_range, R);
+          r0 = __shfl_sync(0xffffffffu, r0, 0);
+          if (r0 >= total) break;
+          const int r1 = min(total, r0 + R);
+          if (sweep == 0) {
+            tile_range_items<U>(g, seg_pre, seg_off, ncomp, r0, r1,
+                                [&](int k, int64_t, int x, unsigned) {
+                                  if (k >= 0) {
+                                    const int xr = x - X;
+                                    atomicAdd(&tile[xr >> 1], 1u << ((xr & 1) << 4));
+                                  }
+                                });
+          } else {
+            tile_range_items<U>(g, seg_pre, seg_off, ncomp, r0, r1,
+                                [&](int k, int64_t q, int x, unsigned M) {
+              SumT c = 0;
+              if (k >= 0) {
+                c = (SumT)((unsigned)tile16[x - X] - 1u);
+                if (c) red_add(&c4s[q], (CT)c);  // edge w-x
+              }
+              // per-run sums of the step (runs of one segment end where the
+              // next lane starts a segment): inclusive warp scan, minus the
+              // scan value just before the run; the run's last lane adds it
+              SumT incl = c;
+#pragma unroll
+              for (int off = 1; off < 32; off <<= 1) {
+                const SumT v = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += v;
+              }
+              const unsigned start = M & (0xffffffffu >> (31 - lane));  // run start <= lane
+              const int rs = start ? 31 - __clz(start) : 0;
+              const SumT before = __shfl_sync(0xffffffffu, incl, rs > 0 ? rs - 1 : 0);
+              const SumT run = incl - (rs > 0 ? before : (SumT)0);
+              const int kn = __shfl_down_sync(0xffffffffu, k, 1);
+              const bool end = lane == 31 || ((M >> (lane + 1)) & 1u) || kn != k;
+              if (k >= 0 && end && run) atomicAdd(&seg_sum[k], run);
+            });
+          }
+        }
+        __syncthreads();
+        if (sweep && threadIdx.x < ncomp) {
+          const SumT sm = seg_sum[threadIdx.x];
+          if (sm) {
+            red_add(&c4s[b + seg_slot[threadIdx.x]], (CT)sm);  // edge s-w
+            local += (u64)sm;
+          }
+        }
+      }
+    }
+    if (!per_edge) {  // 2*C(c,2) over the tile's counters
+      for (int i = threadIdx.x; i < P.T / 8; i += NT) {
+        const uint4 w4 = t4[i];
+        const unsigned wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+          const u64 c0 = wv[t] & 0xffffu, c1 = wv[t] >> 16;
+          local += c0 * (c0 - (c0 > 0)) + c1 * (c1 - (c1 > 0));
+        }
+      }
+    }
+    __syncthreads();
+    const u64 sum = BR(tmp.red).Sum(local);
+    if (threadIdx.x == 0 && sum) atomic_add_u128(c4tot2 + 2 * graph_of(g, s), sum);
+  }
+}
+
 // number of isolated vertices: they hold the lowest ranks (degree 0)
 __global__ void k_isolated(View g, int* __restrict__ out) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1513,7 +1760,8 @@ void set_smem(K kernel, size_t bytes) {
 // against the oracle on small graphs.  Results never depend on the path.
 struct ForcePaths {
   bool tri_gmem = false, tri_small = false, tri_blocks = false, c4_smem = false,
-       c4_coop = false, c4_hub32 = false, c4_flow = false;
+       c4_coop = false, c4_hub32 = false, c4_flow = false, c4_cluster = false,
+       c4_tile64 = false;
 };
 
 ForcePaths read_force() {
@@ -1530,6 +1778,10 @@ ForcePaths read_force() {
   // heavy-frame schedulers on any graph size: cluster path off, two frames
   // per round (many rounds, every slab set reused)
   f.c4_flow = v.find("c4_flow") != std::string::npos;
+  // heavy frames on the (older) DSMEM cluster kernel, or on x-tiles of 64
+  // counters (every frame cut into many tiles)
+  f.c4_cluster = v.find("c4_cluster") != std::string::npos;
+  f.c4_tile64 = v.find("c4_tile64") != std::string::npos;
   return f;
 }
 
@@ -1854,6 +2106,19 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       }
     }
     n32 = (int64_t)f32_all.size();
+    // counters cover ranks [x0, n): isolated vertices (the lowest ranks)
+    // never end a wedge
+    int x0 = 0;
+    if (!f16_all.empty()) {
+      int* d0 = ws_get<int>(g, "x0", 1, s);
+      GD_CUDA(cudaMemsetAsync(d0, 0, 4, s));
+      k_isolated<<<grid_cap(n, 256), 256, 0, s>>>(v, d0);
+      GD_LAUNCH_CHECK("isolated");
+      GD_CUDA(cudaMemcpyAsync(&x0, d0, 4, cudaMemcpyDeviceToHost, s));
+      GD_CUDA(cudaStreamSynchronize(s));
+      x0 &= ~1;
+    }
+    const bool use_tiles = !force.c4_flow && !force.c4_cluster && env_int("GD_C4_TILES", 1) != 0;
     for (const int rk : my_ranks) {
     // this shard's frames: every world-th heavy frame in descending-work order
     std::vector<int> f16, f32;
@@ -1869,7 +2134,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     // clusters measured slower than the L2 rounds: hot counters serialise
     // on one SM's shared memory and only 7 16-CTA clusters are resident)
     int csize = 0, per = 0;
-    if (env_int("GD_C4_CLUSTER", 1) && !force.c4_flow) {
+    if (force.c4_cluster || (env_int("GD_C4_CLUSTER", 1) && !force.c4_flow && !use_tiles)) {
       const int64_t max_per = 98304;  // u16 counters per CTA (192 KB)
       const int cmax = (int)env_int("GD_C4_CLUSTER_MAX", 4);
       for (int c = 1; c <= cmax; c *= 2) {
@@ -1881,7 +2146,48 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
         }
       }
     }
-    if (!f16.empty() && csize) {
+    if (!f16.empty() && use_tiles) {
+      constexpr int NT = 1024;
+      const int T = force.c4_tile64 ? 64 : (int)(env_int("GD_C4_TILE", 90112) & ~int64_t(7));
+      const int64_t ptot = (n - x0 + T - 1) / T;
+      const int P1 = (int)ptot + 1;
+      int64_t* TS = ws_get<int64_t>(g, "c4_ts", (size_t)n * P1, s);
+      k_tile_splits<<<grid_cap(n * 32, 256), 256, 0, s>>>(v, x0, T, P1, TS);
+      GD_LAUNCH_CHECK("tile_splits");
+      std::vector<int64_t> jpre(f16.size() + 1, 0);
+      for (size_t j = 0; j < f16.size(); j++)
+        jpre[j + 1] = jpre[j] + (int64_t)((f16[j] - 1 - x0) / T + 1);
+      std::vector<int> jframe(jpre.back());
+      for (size_t j = 0; j < f16.size(); j++)
+        std::fill(jframe.begin() + jpre[j], jframe.begin() + jpre[j + 1], (int)j);
+      DBuf<int> dfr, djf;
+      DBuf<int64_t> djp;
+      DBuf<unsigned long long> njob;
+      dfr.alloc(f16.size(), s);
+      djp.alloc(jpre.size(), s);
+      djf.alloc(jframe.size(), s);
+      njob.alloc(1, s);
+      njob.zero();
+      GD_CUDA(cudaMemcpyAsync(dfr.p, f16.data(), f16.size() * 4, cudaMemcpyHostToDevice, s));
+      GD_CUDA(cudaMemcpyAsync(djp.p, jpre.data(), jpre.size() * 8, cudaMemcpyHostToDevice, s));
+      GD_CUDA(cudaMemcpyAsync(djf.p, jframe.data(), jframe.size() * 4, cudaMemcpyHostToDevice, s));
+      TilePlan TP{dfr.p, djp.p, djf.p, (int)f16.size(), jpre.back(), x0, T, P1, TS};
+      const size_t sm = (size_t)T * 2;
+      auto tk = k_c4_tiles<NT, u64>;
+      auto tk32 = k_c4_tiles<NT, unsigned>;
+      set_smem(tk, sm);
+      set_smem(tk32, sm);
+      int occ = 0;
+      GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tk, NT, sm));
+      if (occ < 1) throw Error(GD_ECUDA, "c4 tile kernel cannot be resident");
+      const int grid = (int)std::min<int64_t>(jpre.back(), (int64_t)occ * num_sms());
+      if (narrow)
+        tk32<<<grid, NT, sm, s>>>(v, WP.p, TP, pe, (unsigned*)c4s_p, c4tot2.p, njob.p);
+      else
+        tk<<<grid, NT, sm, s>>>(v, WP.p, TP, pe, c4s_p, c4tot2.p, njob.p);
+      GD_LAUNCH_CHECK("c4_tiles");
+      nrounds += jpre.back();  // reported: tile jobs
+    } else if (!f16.empty() && csize) {
       constexpr int NT = 512;
       const size_t sm = (size_t)per * 2;
       auto kern = k_c4_cluster<NT, u64>;
@@ -1909,18 +2215,18 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       if (nclusters < 1) throw Error(GD_ECUDA, "cluster kernel cannot be resident");
       cfg.gridDim = dim3(nclusters * csize);
       DBuf<int> dfr, queue;
-      dfr.alloc(f16_all.size(), s);
+      // this shard's own frames (f16), walked as shard 0 of 1
+      dfr.alloc(f16.size(), s);
       queue.alloc(1, s);
       queue.zero();
-      GD_CUDA(cudaMemcpyAsync(dfr.p, f16_all.data(), f16_all.size() * 4, cudaMemcpyHostToDevice,
-                              s));
+      GD_CUDA(cudaMemcpyAsync(dfr.p, f16.data(), f16.size() * 4, cudaMemcpyHostToDevice, s));
       if (narrow)
         GD_CUDA(cudaLaunchKernelEx(&cfg, kern32, v, (const int64_t*)WP.p, (const int*)dfr.p,
-                                   (int)f16_all.size(), rk, world, queue.p, per, pe,
+                                   (int)f16.size(), 0, 1, queue.p, per, pe,
                                    (unsigned*)c4s_p, c4tot2.p));
       else
         GD_CUDA(cudaLaunchKernelEx(&cfg, kern, v, (const int64_t*)WP.p, (const int*)dfr.p,
-                                   (int)f16_all.size(), rk, world, queue.p, per, pe, c4s_p,
+                                   (int)f16.size(), 0, 1, queue.p, per, pe, c4s_p,
                                    c4tot2.p));
       GD_LAUNCH_CHECK("c4_cluster");
       nrounds = -csize;  // reported as the cluster size
@@ -1936,18 +2242,6 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fk, fnt, 0));
       if (per_sm < 1) throw Error(GD_ECUDA, "c4 flow kernel cannot be resident");
       const int grid = per_sm * num_sms();
-      // counters cover ranks [x0, n): isolated vertices (the lowest ranks)
-      // never end a wedge
-      int x0 = 0;
-      {
-        int* d0 = ws_get<int>(g, "x0", 1, s);
-        GD_CUDA(cudaMemsetAsync(d0, 0, 4, s));
-        k_isolated<<<grid_cap(n, 256), 256, 0, s>>>(v, d0);
-        GD_LAUNCH_CHECK("isolated");
-        GD_CUDA(cudaMemcpyAsync(&x0, d0, 4, cudaMemcpyDeviceToHost, s));
-        GD_CUDA(cudaStreamSynchronize(s));
-        x0 &= ~1;
-      }
       const int64_t slab_words = ((((int64_t)n - x0) + 1) / 2 + 31) & ~int64_t(31);
       const int64_t l2_budget = env_int("GD_C4_FLOW_MB", 640) << 20;  // all slab sets
       // a round's use (or scan) tasks are handed out LU steps after its count

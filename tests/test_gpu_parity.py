@@ -11,6 +11,7 @@ import pytest
 
 import paper_1506_04322_b200 as gd
 from helpers import GOLDEN, configs, int_counts, sha, small_graphs
+from sample_sets import count_rows_from_table, count_sample
 from oracle import oracle as O
 from paper_1506_04322_b200 import workloads as W
 
@@ -61,7 +62,9 @@ def test_degenerate_graphs():
 
 
 FORCED = ["tri_gmem", "tri_small", "tri_blocks", "c4_coop", "c4_hub32", "c4_smem",
-          "c4_flow", "tri_gmem,c4_coop", "tri_small,c4_hub32", "wide_slots", "c4_flow,wide_slots"]
+          "c4_flow", "tri_gmem,c4_coop", "tri_small,c4_hub32", "wide_slots", "c4_flow,wide_slots",
+          "c4_tile64", "c4_coop,c4_tile64", "c4_coop,c4_tile64,wide_slots", "c4_coop,c4_cluster",
+          "c4_coop,c4_flow"]
 
 
 def _dense_cases():
@@ -169,28 +172,53 @@ def test_config4_batch_feature_matrix():
     assert np.array_equal(fm3.rows, gold["counts"][:16].astype(np.float64))
 
 
-def _big_parity(name, sample):
+def _chunk_sha(a, rows):
+    a = np.ascontiguousarray(a)
+    return [sha(a[i:i + rows]) for i in range(0, len(a), rows)]
+
+
+def _big_parity(name, live_sample):
+    """Full-size parity of a config:
+    * every row of the device per-edge table against the independent CPU
+      cross-check (tests/golden/crosscheck_<cfg>.json, one sha256 per 65536
+      rows; the cross-check is itself pinned to the literal oracle and the
+      reference, tests/test_crosscheck.py);
+    * the literal oracle's _micro_edge rows of the survey sample (uniform +
+      top-1k by w_e + top-100-hub edges) and its _count_edge rows of 1M
+      uniform edges (oracle_<cfg>_{micro,count}_sample, tools/make_big_fixtures.py);
+    * a live oracle sample computed here, global counts against the full
+      C-oracle census (C3) and the cross-check (C3, C5), and the two device
+      routes / validate() identities."""
+    import json
     raw = W.config_graph(name)
     g = gd.Graph.from_edges(raw.pairs, _declared_n=raw.n)
     f = gd.graphlet_census(g)
     tab, f2 = gd.micro_census_table(g)
+    tab = np.asarray(tab)
     assert f2 == f  # two device routes (global closure vs per-edge sums)
     assert gd.frequencies_from_micro(g, tab) == f  # dual route over the table
     f.validate()
     edges = np.asarray(g.edges)
+    xc = json.loads((GOLDEN / f"crosscheck_{name}.json").read_text())
+    assert xc["m"] == g.m and sha(edges) == xc["edges_sha256"]
+    assert f.counts == int_counts(xc["counts"])
+    got = _chunk_sha(tab, xc["chunk_rows"])
+    bad = [i for i, (a, b) in enumerate(zip(got, xc["chunk_sha256"])) if a != b]
+    assert len(got) == len(xc["chunk_sha256"]) and not bad, \
+        f"{len(bad)} of {len(got)} table chunks differ, first rows {bad[:1] and bad[0] * xc['chunk_rows']}"
+    z = np.load(GOLDEN / f"oracle_{name}_micro_sample.npz")
+    assert str(z["edges_sha256"]) == xc["edges_sha256"]
+    assert np.array_equal(tab[z["idx"]], z["rows"])
+    cs = json.loads((GOLDEN / f"oracle_{name}_count_sample.json").read_text())
+    idx = count_sample(g.m, cs["k"])
+    assert sha(idx) == cs["idx_sha256"]
+    assert _chunk_sha(count_rows_from_table(tab, idx), cs["chunk"]) == cs["chunk_sha256"]
+    # a live literal-oracle sample on this box (independent of the fixtures)
     rng = np.random.default_rng(2024)
-    idx = rng.choice(g.m, sample, replace=False)
-    # plus the heaviest edges (largest max-endpoint degree)
-    deg = np.asarray(g.degrees)
-    heavy = np.argsort(-np.maximum(deg[edges[:, 0]], deg[edges[:, 1]]), kind="stable")[:64]
-    idx = np.unique(np.concatenate([idx, heavy]))
-    assert np.array_equal(np.asarray(tab)[idx], O.micro_rows(edges, g.n, idx))
-    gold = configs().get(name)
-    if gold and "counts" in gold:
-        assert f.counts == int_counts(gold["counts"])
+    idx = rng.choice(g.m, live_sample, replace=False)
+    assert np.array_equal(tab[idx], O.micro_rows(edges, g.n, idx))
     full = GOLDEN / f"oracle_{name}.json"  # full census by the C oracle (tools/)
     if full.exists():
-        import json
         d = json.loads(full.read_text())
         assert d["m"] == g.m and f.counts == int_counts(d["counts"])
     return g, f
