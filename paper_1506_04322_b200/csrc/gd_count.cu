@@ -1875,16 +1875,23 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
 
   // ---- pass A / pass B: triangle frames by D = |N+(a)| ----------------------
   const int64_t maxD = n ? dk.value(0) : 0;
-  // graph-wide hit buffer (per-edge mode): exact-size lists for pass B,
-  // capacity = min(sum_a min(items_a, C(D_a, 2)), 60% of free memory)
+  // graph-wide hit buffer (per-edge mode): exact-size lists for pass B.
+  // Capacity = min(sum_a min(items_a, C(D_a, 2)) -- cached per graph --, 60% of
+  // the memory this process can still allocate (device free memory plus the
+  // unused reserve of the stream-ordered pool)).  The buffer lives for this
+  // census only (returned to the pool, so other censuses and builds can use
+  // it); if the allocation fails -- e.g. concurrent censuses on several host
+  // threads -- the capacity is halved, and at worst pass B re-probes every
+  // frame (hit_cap = 0): slower, never wrong.
   const bool lists = env_int("GD_TRI_LISTS", 1) != 0;
+  DBuf<u64> hitbuf_mem;
   u64* hitbuf = nullptr;
   u64* hittop = nullptr;
   int64_t* hoff = nullptr;
   int* hcnt = nullptr;
   u64 hit_cap = 0;
   if (per_edge && lists && n) {
-    if (!g.hit_cap_known) {  // sized once per graph: min(bound, 40% of the device)
+    if (!g.hit_cap_known) {
       DBuf<u64> bound;
       bound.alloc(1, s);
       bound.zero();
@@ -1893,14 +1900,37 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       u64 hb = 0;
       GD_CUDA(cudaMemcpyAsync(&hb, bound.p, 8, cudaMemcpyDeviceToHost, s));
       GD_CUDA(cudaStreamSynchronize(s));
-      size_t fr = 0, tot = 0;
-      GD_CUDA(cudaMemGetInfo(&fr, &tot));
-      g.hit_cap = std::min<u64>(hb, (u64)(tot * 0.4) / 8);
+      g.hit_cap = hb;
       g.hit_cap_known = true;
     }
-    hit_cap = std::min<u64>(g.hit_cap, (u64)env_int("GD_HIT_CAP", INT64_MAX));  // tests
+    size_t fr = 0, tot = 0;
+    GD_CUDA(cudaMemGetInfo(&fr, &tot));
+    u64 spare = 0;
+    {
+      int dev = 0;
+      cudaMemPool_t pool;
+      uint64_t res = 0, used = 0;
+      if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess &&
+          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res) == cudaSuccess &&
+          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess &&
+          res > used)
+        spare = res - used;
+    }
+    hit_cap = std::min<u64>(g.hit_cap, (u64)((fr + spare) * 0.6) / 8);
+    hit_cap = std::min<u64>(hit_cap, (u64)env_int("GD_HIT_CAP", INT64_MAX));  // tests
+    while (hit_cap) {
+      void* p = nullptr;
+      if (cudaMallocAsync(&p, hit_cap * 8, s) == cudaSuccess) {
+        hitbuf_mem.p = (u64*)p;
+        hitbuf_mem.n = hit_cap;
+        hitbuf_mem.s = s;
+        break;
+      }
+      cudaGetLastError();  // out of memory: try half, then fall back to probing
+      hit_cap = hit_cap > (1u << 20) ? hit_cap / 2 : 0;
+    }
     if (hit_cap) {
-      hitbuf = ws_get<u64>(g, "hitbuf", hit_cap, s);
+      hitbuf = hitbuf_mem.p;
       hittop = ws_get<u64>(g, "hittop", 1, s);
       GD_CUDA(cudaMemsetAsync(hittop, 0, 8, s));
       hoff = ws_get<int64_t>(g, "hoff", n, s);
@@ -2118,7 +2148,15 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       GD_CUDA(cudaStreamSynchronize(s));
       x0 &= ~1;
     }
-    const bool use_tiles = !force.c4_flow && !force.c4_cluster && env_int("GD_C4_TILES", 1) != 0;
+    // x-tiles in shared memory: always for the global census (its count
+    // sweep is the whole job); per edge only while a frame spans few tiles --
+    // the use sweep then walks each lower row in per-tile pieces, which at
+    // n = 4M (43 tiles, ~22 items per piece) costs more than the dense L2
+    // slabs save (C5 per-edge flow 474 -> 549 ms, C3 48.3 -> 43.0 ms)
+    const int64_t tile_mode = env_int("GD_C4_TILES", 1);
+    const int64_t max_tiles = (n - x0 + 90111) / 90112;
+    const bool use_tiles = !force.c4_flow && !force.c4_cluster && tile_mode != 0 &&
+                           (tile_mode == 2 || force.c4_tile64 || !per_edge || max_tiles <= 16);
     for (const int rk : my_ranks) {
     // this shard's frames: every world-th heavy frame in descending-work order
     std::vector<int> f16, f32;
