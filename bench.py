@@ -150,19 +150,76 @@ def measured_peak():
 
 
 def ncu_traffic(config: str, mode: str):
-    """DRAM bytes (read + write) of one census, summed over its kernels, and
-    the top kernel with its time share, from the committed ncu launch list
-    summary (profiles/ncu_summary.json, made by tools/ncu_sum.py)."""
+    """(DRAM bytes of the top kernel per launch, its name / share, DRAM bytes
+    of one whole census) from the committed ncu launch-list summary
+    (profiles/ncu_summary.json, made by tools/ncu_sum.py)."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
-        return None, None
+        return None, None, None
     try:
         e = json.loads(p.read_text())[f"{config}/{mode}"]
         top = next(iter(e["kernels"].items()))
-        return e["census_dram_bytes"], {"name": top[0], "share": top[1]["share"],
-                                        "dram_bytes": top[1]["dram_bytes"]}
+        per = top[1]["dram_bytes"] / max(1, top[1]["launches"])
+        return per, {"name": top[0], "share": top[1]["share"], "dram_bytes": per}, \
+            e["census_dram_bytes"]
     except (KeyError, ValueError, StopIteration):
-        return None, None
+        return None, None, None
+
+
+def roofline_block(config, mode, phases, stats, n, m, deg, ms, peak, peak_kind) -> dict:
+    """Roofline of the dominant kernel.
+
+    achieved = algorithmic bytes of one launch / its live CUDA-event time.
+    The algorithmic bytes are the item stream of the frame / wedge algorithm
+    (what it must move through the memory system if nothing were cached):
+      pass C heavy frames: 4 B (col[] entry of the wedge's end x) per heavy
+        wedge per sweep, plus in per-edge mode a 4 B slot update per wedge
+        (count + use sweeps: 12 B / wedge; global: 4 B / wedge);
+      pass A triangle frames: 4 B per frame item (col[] entry probed).
+    traffic = the ncu-measured DRAM bytes of that kernel (profiles/
+    ncu_summary.json, same code); hbm_measured turns traffic into the HBM
+    fraction actually used (always <= 1); compulsory = CSR read once + per-edge
+    table written once; effective = SURVEY 8(d)'s B_alg over the census time
+    (the per-edge formulation's bytes, which this algorithm never reads, so it
+    may exceed 1 and is not a bound)."""
+    per_edge = mode == "per_edge"
+    traffic, ncu_kernel, census_dram = ncu_traffic(config, mode)
+    wh = stats.get("c4_heavy_wedges", 0)
+    items = stats.get("tri_items", 0)
+    models = {
+        "c4_coop": (4 * wh * (3 if per_edge else 1),
+                    f"{wh} heavy wedges x {'(4 B col per sweep x 2 + 4 B slot update)' if per_edge else '4 B col'}"),
+        "tri_frames": (4 * items, f"{items} frame items x 4 B col"),
+    }
+    dom = max(((k, v) for k, v in phases.items() if k in models), key=lambda kv: kv[1],
+              default=("", 0.0))
+    alg, model = models.get(dom[0], (0, ""))
+    t = max(dom[1], 1e-9) / 1e3
+    achieved = alg / t / 1e9
+    sum_d2 = int(np.dot(deg, deg))
+    b_alg = m * (8 + 4 * 8 + 8 * (10 if per_edge else 0)) + 4 * sum_d2
+    compulsory = 8 * (n + 1) + 8 * m * 2 + (80 * m if per_edge else 0)
+    out = {"bound": "hbm", "kernel": (ncu_kernel or {}).get("name", dom[0]), "phase": dom[0],
+           "phase_ms": dom[1], "share_of_census": dom[1] / max(ms, 1e-9),
+           "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+           "algorithmic_bytes": alg, "model": model, "traffic": traffic,
+           "peak_source": peak_kind}
+    if traffic:
+        out["hbm_measured"] = {
+            "kernel_gbs": traffic / t / 1e9, "kernel_frac": traffic / t / 1e9 / peak,
+            "census_gbs": census_dram / (ms / 1e3) / 1e9 if census_dram else None,
+            "census_frac": census_dram / (ms / 1e3) / 1e9 / peak if census_dram else None,
+            "source": "ncu dram__bytes_read.sum + dram__bytes_write.sum (profiles/ncu_summary.json)"
+                      " over this run's CUDA-event time"}
+    out["compulsory"] = {"bytes": compulsory, "gbs": compulsory / (ms / 1e3) / 1e9,
+                         "frac": compulsory / (ms / 1e3) / 1e9 / peak,
+                         "model": "CSR offsets + neighbour lists read once" +
+                                  (", int64 (m, 10) table written once" if per_edge else "")}
+    out["effective_b_alg"] = {"bytes": b_alg, "gbs": b_alg / (ms / 1e3) / 1e9,
+                              "frac_effective": b_alg / (ms / 1e3) / 1e9 / peak,
+                              "model": "SURVEY 8(d): m(8+4o+8K) + 4 sum d^2 (both adjacency "
+                                       "lists per edge; not read by this algorithm)"}
+    return out
 
 
 def load_graph(config: str):
@@ -209,6 +266,7 @@ def cpu_baseline(raw, mode: str, budget_s: float) -> dict:
     t, kk = cpu_sample_run(og, mode, k, seed=7)
     full = t * og.m / kk
     return {"value": og.m / full, "unit": "edges/s", "cores": os.cpu_count(), "kind": "port",
+            "extrapolated": True,
             "sample": f"{kk} uniformly sampled edge jobs of the {og.m}-edge graph "
                       f"({'_micro_edge' if mode == 'per_edge' else '_count_edge'} C restatement, "
                       f"{os.cpu_count()} OpenMP threads) in {t:.2f} s; full census "
@@ -237,7 +295,7 @@ def run_reference(args, rank: int, world: int):
         "config": {"workload": args.config, "mode": args.mode, "graph": CONFIG_DESC[args.config],
                    "n": og.n, "m": og.m, "parallelism": "cpu threads"},
         "cpu_baseline": {"value": value, "unit": "edges/s", "cores": os.cpu_count(),
-                         "kind": "port",
+                         "kind": "port", "extrapolated": True,
                          "sample": f"each step: {k} uniformly sampled edge jobs, full census "
                                    f"time extrapolated x m/k"},
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0,
@@ -339,51 +397,48 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     deg = np.asarray(g.degrees, dtype=np.int64)
     del g
     # --- end to end through the public API (host memory both ways) ----------
+    # headline: the drop-in default call a user makes, from the pageable
+    # numpy pairs the generator returned -> Graph.from_edges -> micro_table
+    # (a fresh int64 table every step, returned as a numpy array; the library
+    # recycles the page-locked blocks of tables the caller has dropped).
+    # Beside it: the same calls from page-locked pairs into a reused output.
     dist.barrier()
-    e2e_ms = []
-    # the e2e leg gets the same W untimed warm-up steps as the resident leg
-    # (measured with GD_BENCH_DEBUG=1: the first two fresh graphs after the
-    # resident phase build in 300-450 ms, every later one in 12-17 ms)
     e2e_warm = max(1, args.warmup)
-    for i in range(args.steps + e2e_warm):
-        t0 = time.perf_counter()
-        g2 = gd.Graph.from_edges(pairs, gd.ParseOptions(num_vertices=raw.n))
-        tb = time.perf_counter()
-        f2 = census(g2, out=htab if per_edge else None)
-        tc = time.perf_counter()
-        dev = sum(gd.last_timings(g2).values()) if DEBUG else 0.0
-        del g2
-        dt = (time.perf_counter() - t0) * 1e3
-        if DEBUG:  # NVML (no CUDA context of its own) for the device memory in use
-            import pynvml
-            pynvml.nvmlInit()
-            used = pynvml.nvmlDeviceGetMemoryInfo(pynvml.nvmlDeviceGetHandleByIndex(local_rank)).used
-            ps = (ctypes.c_uint64 * 4)()
-            L.gd_pool_stats(ps)
-            print(f"e2e step {i}: build {1e3 * (tb - t0):.1f} census {1e3 * (tc - tb):.1f} "
-                  f"(device {dev:.1f}) free {1e3 * (time.perf_counter() - tc):.1f} "
-                  f"gpu used {used / 2**30:.2f} GiB pool reserved {ps[0] / 2**30:.2f} "
-                  f"(high {ps[1] / 2**30:.2f}) used {ps[2] / 2**30:.2f} "
-                  f"(high {ps[3] / 2**30:.2f}) GiB", file=sys.stderr, flush=True)
-        if i >= e2e_warm:
-            e2e_ms.append(dt)
-        if f2 != f_ref:
-            raise SystemExit("end-to-end census differs from the resident one")
+
+    def e2e_leg(src, out):
+        times = []
+        for i in range(args.steps + e2e_warm):
+            t0 = time.perf_counter()
+            g2 = gd.Graph.from_edges(src, gd.ParseOptions(num_vertices=raw.n))
+            if comm is not None or not per_edge:
+                f2 = census(g2, out=out if per_edge else None)
+                tab2 = None
+            elif out is None:
+                tab2, f2 = gd.micro_census_table(g2)
+            else:
+                tab2, f2 = gd.micro_census_table(g2, out=out)
+            dt = (time.perf_counter() - t0) * 1e3
+            if DEBUG:
+                print(f"e2e step {i}: {dt:.1f} ms (device {sum(gd.last_timings(g2).values()):.1f})",
+                      file=sys.stderr, flush=True)
+            del g2, tab2
+            if i >= e2e_warm:
+                times.append(dt)
+            if f2 != f_ref:
+                raise SystemExit("end-to-end census differs from the resident one")
+        return times
+
+    e2e_ms = e2e_leg(raw.pairs, None)
+    e2e_pin_ms = e2e_leg(pairs, htab)
     dist.barrier()
-    # median over steps (median of the runs); the mean, which
-    # host-side outliers of the box move (an occasional +100-300 ms step with
-    # unchanged device time), is reported beside it
+    # median over steps (median of the runs); mean and max beside it
     e2e = dist.max(statistics.median(e2e_ms))
     e2e_mean = dist.max(statistics.mean(e2e_ms))
+    e2e_pin = dist.max(statistics.median(e2e_pin_ms))
 
-    # --- roofline: SURVEY 8(d) algorithmic bytes of one census ---------------
-    sum_d2 = int(np.dot(deg, deg))
-    o_bytes, k_out = 8, (10 if per_edge else 0)
-    b_alg = m * (8 + 4 * o_bytes + 8 * k_out) + 4 * sum_d2
+    # --- roofline -----------------------------------------------------------
     peak, peak_kind = measured_peak()
-    achieved = b_alg / (ms / 1e3) / 1e9
-    traffic, ncu_kernel = ncu_traffic(args.config, args.mode)
-    dom = max(phases.items(), key=lambda kv: kv[1]) if phases else ("", 0.0)
+    roof = roofline_block(args.config, args.mode, phases, stats, n, m, deg, ms, peak, peak_kind)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -409,25 +464,22 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                        else "single",
                        "l2": "flushed between steps (256 MiB device memset)",
                        "timing": "CUDA events on the library stream, whole census"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": peak_kind,
-                         "algorithmic_bytes": b_alg,
-                         "kernel": "census pipeline (B_alg of SURVEY 8(d) / summed kernel time)",
-                         "dominant_phase": dom[0],
-                         "dominant_share": dom[1] / max(ms, 1e-9),
-                         "ncu_kernel": ncu_kernel,
-                         # the dominant phase's kernel: ncu DRAM bytes of one
-                         # launch over its live CUDA-event time in this run
-                         "dominant_dram_gbs": (ncu_kernel["dram_bytes"] / (dom[1] / 1e3) / 1e9
-                                               if ncu_kernel and dom[1] > 0 else None)},
+            "roofline": roof,
             "phases_ms": {k: round(v, 3) for k, v in phases.items()},
             "work": {k: v for k, v in stats.items() if k != "launches"},
             "wall_ms_per_step": wall_ms,
             "e2e": {"value": m / (e2e / 1e3), "unit": "edges/s", "ms_per_step": e2e,
-                    "ms_mean": e2e_mean, "ms_steps": [round(x, 2) for x in e2e_ms],
-                    "h2d_bytes_per_step": int(pairs.nbytes),
-                    "d2h_bytes_per_step": int((m * 80 if per_edge else 0) + 13 * 16 + 8)},
+                    "ms_mean": e2e_mean, "ms_max": max(e2e_ms),
+                    "ms_steps": [round(x, 2) for x in e2e_ms],
+                    "call": "micro_table(Graph.from_edges(pairs)) from pageable numpy pairs, "
+                            "fresh int64 table returned every step" if per_edge else
+                            "graphlet_census(Graph.from_edges(pairs)) from pageable numpy pairs",
+                    "h2d_bytes_per_step": int(raw.pairs.nbytes),
+                    "d2h_bytes_per_step": int((m * 80 if per_edge else 0) + 13 * 16 + 8),
+                    "pinned": {"value": m / (e2e_pin / 1e3), "ms_per_step": e2e_pin,
+                               "ms_steps": [round(x, 2) for x in e2e_pin_ms],
+                               "call": "page-locked pairs, output into a reused page-locked "
+                                       "table (micro_census_table(out=...))"}},
             "gpu_launches": launches,
             "clocks": clk,
             "cpu_baseline": cpu,
@@ -457,7 +509,6 @@ def bench_resident_config(gd, N, L, config: str, peak: float, steps: int = 3,
     del raw
     n, m = g.n, g.m
     deg = np.asarray(g.degrees, dtype=np.int64)
-    sum_d2 = int(np.dot(deg, deg))
     dtab = L.gd_device_alloc(m * 10 * 8)
     out = {"workload": config, "graph": CONFIG_DESC[config], "n": n, "m": m,
            "steps": steps, "warmup": warmup,
@@ -478,11 +529,11 @@ def bench_resident_config(gd, N, L, config: str, peak: float, steps: int = 3,
                 if i >= warmup:
                     ms.append(sum(gd.last_timings(g).values()))
             t = statistics.mean(ms)
-            b_alg = m * (8 + 4 * 8 + 8 * (10 if mode == "per_edge" else 0)) + 4 * sum_d2
+            ph = gd.last_timings(g)
             out[mode] = {"ms_per_step": t, "value": m / (t / 1e3), "unit": "edges/s",
-                         "roofline_frac": b_alg / (t / 1e3) / 1e9 / peak,
-                         "algorithmic_bytes": b_alg,
-                         "phases_ms": {k: round(v, 3) for k, v in gd.last_timings(g).items()}}
+                         "roofline": roofline_block(config, mode, ph, gd.last_stats(g), n, m,
+                                                    deg, t, peak, "measured"),
+                         "phases_ms": {k: round(v, 3) for k, v in ph.items()}}
         if out["per_edge"] and ref is not None:
             out["g4_4"] = str(ref.counts["g4_4"])
     finally:

@@ -12,12 +12,13 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 BUILD = PKG / "_build_obj"
 LIB = PKG / "libgdgpu.so"
-SOURCES = ("gd_build.cu", "gd_count.cu", "gd_parse.cu", "gd_derive.cu", "gd_rank.cu", "gd_select.cu", "gd_api.cu")
+SOURCES = ("gd_build.cu", "gd_count.cu", "gd_parse.cu", "gd_derive.cu", "gd_rank.cu",
+           "gd_select.cu", "gd_copy.cu", "gd_api.cu")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",
     "-gencode", "arch=compute_100a,code=sm_100a",
-    "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-Xcompiler", "-fopenmp",
     "--expt-relaxed-constexpr",
     f"-I{PKG.parent / 'include'}",
 ]
@@ -57,7 +58,7 @@ def build(verbose: bool = False, force: bool = False, defines=(), lib: Path = LI
     if force or jobs or not LIB.exists():
         tmp = LIB.with_suffix(".so.tmp")
         cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
-               *map(str, objs), "-o", str(tmp), "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+               *map(str, objs), "-o", str(tmp), "-lcudart_static", "-lrt", "-ldl", "-lpthread", "-lgomp"]
         run(cmd)
         os.replace(tmp, LIB)
     return LIB

@@ -164,34 +164,89 @@ def wide(sums: np.ndarray) -> list[int]:
     return [int(lo) + (int(hi) << 64) for lo, hi in s]
 
 
-class _PinnedBuffer:
-    """Owns page-locked host memory from gd_host_alloc.  Exposed to numpy via
-    __array_interface__, so every numpy view's base chain ends here and the
-    memory is freed only when the last view is gone."""
+class _PinnedPool:
+    """Library-owned cache of page-locked host blocks.  cudaHostAlloc of a
+    per-edge table (1.26 GB at R-MAT-20) costs tens of milliseconds and its
+    cudaFreeHost synchronises the device, so blocks released by the arrays
+    that used them are kept (up to ``GD_PINNED_CACHE_MB``, default 16 GiB)
+    and handed to the next request of the same or a slightly smaller size."""
 
-    def __init__(self, p: int, nbytes: int, free):
+    def __init__(self):
+        self.lock = threading.Lock()
+        self.free: list[tuple[int, int]] = []  # (nbytes, pointer)
+        self.cached = 0
+        self.cap = int(os.environ.get("GD_PINNED_CACHE_MB", 16384)) << 20
+
+    def take(self, nbytes: int) -> tuple[int, int]:
+        with self.lock:
+            best = None
+            for i, (size, p) in enumerate(self.free):
+                if nbytes <= size <= 2 * nbytes and (best is None or size < self.free[best][0]):
+                    best = i
+            if best is not None:
+                size, p = self.free.pop(best)
+                self.cached -= size
+                return p, size
+        p = lib().gd_host_alloc(nbytes)
+        if not p:  # pinned memory exhausted: drop the cache and retry once
+            self.trim()
+            p = lib().gd_host_alloc(nbytes)
+        return (p or 0), nbytes
+
+    def give(self, p: int, size: int) -> None:
+        with self.lock:
+            if self.cached + size <= self.cap:
+                self.free.append((size, p))
+                self.cached += size
+                return
+        lib().gd_host_free(p)
+
+    def trim(self) -> None:
+        with self.lock:
+            blocks, self.free, self.cached = self.free, [], 0
+        for _, p in blocks:
+            lib().gd_host_free(p)
+
+
+_pinned_pool = _PinnedPool()
+
+
+class _PinnedBuffer:
+    """Owns one page-locked block of the pool.  Exposed to numpy via
+    __array_interface__, so every numpy view's base chain ends here and the
+    block returns to the pool only when the last view is gone."""
+
+    def __init__(self, p: int, nbytes: int):
         self.p = p
-        self._free = free
+        self.size = nbytes
         self.__array_interface__ = {"data": (p, False), "shape": (nbytes,),
                                     "typestr": "|u1", "version": 3}
 
     def __del__(self):
         if self.p:
-            self._free(self.p)
+            try:
+                _pinned_pool.give(self.p, self.size)
+            except Exception:  # interpreter shutdown
+                pass
             self.p = 0
 
 
 def pinned_empty(shape, dtype=np.int64) -> np.ndarray:
-    """np.empty in page-locked host memory (fast D2H of per-edge tables)."""
+    """np.empty in page-locked host memory from the library's pinned pool
+    (D2H of per-edge tables at full PCIe rate, no per-call pinning)."""
     dtype = np.dtype(dtype)
     count = int(np.prod(shape)) if len(shape) else 1
     nbytes = max(count * dtype.itemsize, 1)
-    L = lib()
-    p = L.gd_host_alloc(nbytes)
+    p, size = _pinned_pool.take(nbytes)
     if not p:
         return np.empty(shape, dtype=dtype)  # pageable is still correct, only slower
-    raw = np.asarray(_PinnedBuffer(p, nbytes, L.gd_host_free))
+    raw = np.asarray(_PinnedBuffer(p, size))
     return raw[:count * dtype.itemsize].view(dtype).reshape(shape)
+
+
+def trim_pinned() -> None:
+    """Release the cached page-locked host blocks."""
+    _pinned_pool.trim()
 
 
 def env_flag(name: str) -> bool:

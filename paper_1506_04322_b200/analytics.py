@@ -16,8 +16,9 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .census import (_STEP_NAMES, batch_counts, census_batch, counts_as_ints,
-                     graphlet_census)
+from . import _native as N
+from .census import (_STEP_NAMES, CensusSums, batch_counts, census_batch, counts_as_ints,
+                     frequencies_from_sums, graphlet_census)
 from .classes import classes_for
 from .frequencies import GraphletFrequencies
 from .graph import GraphBatch
@@ -83,13 +84,30 @@ def feature_matrix(graphs, labels=None, config: ParallelConfig | None = None,
         count = batch.num_graphs if batch is not None else len(graphs)
         if labels is None:
             labels = [f"graph_{i}" for i in range(count)]
+        labels = list(labels)
+        count = min(count, len(labels))  # zip(labels, graphs), reference analytics.py:111
         if count == 0:
             return FeatureMatrix(class_ids, [], np.zeros((0, len(class_ids))), [], [])
         t0 = time.perf_counter()
         if batch is None:
-            batch = GraphBatch.from_graphs(graphs)
-        counts, status = batch_counts(batch)
+            try:
+                batch = GraphBatch.from_graphs(graphs[:count])
+            except Exception:  # a malformed graph: per-graph route, as the reference
+                return feature_matrix(graphs[:count], labels[:count], config, log_scale,
+                                      normalize, census_fn=graphlet_census)
+        counts, status, sums = batch_counts(batch, with_sums=True)
         per = (time.perf_counter() - t0) / count
+        counts, status = counts[:count], status[:count]
+
+        def skip(i):  # the reference's message: the closure re-run on the exact sums
+            try:
+                frequencies_from_sums(CensusSums.from_tuple(N.wide(sums[i])),
+                                      int(batch.n_per_graph[i]), int(batch.m_per_graph[i]))
+                msg = "ConsistencyError: " + _STEP_NAMES[int(status[i]) - 1] + " failed"
+            except Exception as exc:
+                msg = f"{type(exc).__name__}: {exc}"
+            skipped.append((labels[i], msg))
+
         lo, hi = counts[..., 0], counts[..., 1]
         # float(count) exactly as the reference: int64 -> float64 is correctly
         # rounded; the rare counts beyond int64 go through Python ints
@@ -105,15 +123,13 @@ def feature_matrix(graphs, labels=None, config: ParallelConfig | None = None,
             for r in np.nonzero(wide)[0]:
                 matrix[r] = [float(v) for v in counts_as_ints(counts[keep[r]])]
             for i in np.nonzero(~ok)[0]:
-                skipped.append((labels[i], "ConsistencyError: " + _STEP_NAMES[int(status[i]) - 1]
-                                + " failed"))
+                skip(i)
             kept = [labels[i] for i in keep]
             return FeatureMatrix(class_ids, kept, matrix.reshape(len(kept), len(class_ids)),
                                  [per] * len(kept), skipped)
         for i in range(count):
             if status[i]:
-                skipped.append((labels[i], "ConsistencyError: " + _STEP_NAMES[int(status[i]) - 1]
-                                + " failed"))
+                skip(i)
                 continue
             if small[i].all():
                 row = fl[i].tolist()

@@ -207,10 +207,11 @@ _STEP_NAMES = ("triangle closure", "2-star closure", "3-node-1-edge closure",
                "two-edge closure", "one-edge closure", "independent closure")
 
 
-def batch_counts(batch: GraphBatch):
+def batch_counts(batch: GraphBatch, with_sums: bool = False):
     """One device census of every graph of the batch, closed in exact 128-bit
     integers by the library: (counts int64 [G][17][2] as (lo, hi) of signed
-    128-bit values, status [G]: 0 ok, else 1 + failing closure step)."""
+    128-bit values, status [G]: 0 ok, else 1 + failing closure step) and, with
+    ``with_sums``, the raw 13 sums per graph (uint64 [G][26])."""
     G = batch.num_graphs
     sums = np.zeros(G * 2 * N.NUM_SUMS, dtype=np.uint64)
     seen = np.zeros(G, dtype=np.int64)
@@ -224,6 +225,8 @@ def batch_counts(batch: GraphBatch):
     N.check(N.lib().gd_close_counts(N.ptr(sums, ctypes.c_uint64), N.ptr(batch.n_per_graph),
                                     N.ptr(batch.m_per_graph), G, N.ptr(counts),
                                     status.ctypes.data_as(ctypes.POINTER(ctypes.c_int))))
+    if with_sums:
+        return counts, status, sums.reshape(G, 2 * N.NUM_SUMS)
     return counts, status
 
 
@@ -237,14 +240,20 @@ def census_batch(batch: GraphBatch) -> list[GraphletFrequencies | Exception]:
     """Global counts of every graph of a batch from one device pass.  A graph
     whose closure fails yields its ConsistencyError in place of a result."""
     from .classes import CLASS_IDS
-    counts, status = batch_counts(batch)
+    counts, status, sums = batch_counts(batch, with_sums=True)
     out: list = []
     for i in range(batch.num_graphs):
+        n, m = int(batch.n_per_graph[i]), int(batch.m_per_graph[i])
         if status[i]:
-            out.append(ConsistencyError(_STEP_NAMES[int(status[i]) - 1] + " failed"))
+            # the reference's exception and message: the closure re-run on
+            # the exact sums of this graph
+            try:
+                frequencies_from_sums(CensusSums.from_tuple(N.wide(sums[i])), n, m)
+                out.append(ConsistencyError(_STEP_NAMES[int(status[i]) - 1] + " failed"))
+            except Exception as exc:
+                out.append(exc)
             continue
-        f = GraphletFrequencies(counts=dict(zip(CLASS_IDS, counts_as_ints(counts[i]))),
-                                n=int(batch.n_per_graph[i]), m=int(batch.m_per_graph[i]))
+        f = GraphletFrequencies(counts=dict(zip(CLASS_IDS, counts_as_ints(counts[i]))), n=n, m=m)
         out.append(f)
     return out
 
@@ -260,8 +269,10 @@ def last_timings(g) -> dict[str, float]:
 
 def trim_workspace() -> None:
     """Release this thread's cached device workspace of the census kernels
-    (kept between calls so censuses of fresh graphs do not re-allocate)."""
+    (kept between calls so censuses of fresh graphs do not re-allocate) and
+    the cached page-locked host blocks of returned tables."""
     N.check(N.lib().gd_trim_workspace())
+    N.trim_pinned()
 
 
 def last_stats(g) -> dict[str, int]:

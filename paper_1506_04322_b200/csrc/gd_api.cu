@@ -262,9 +262,7 @@ static void census(gd_graph* h, bool per_edge, int64_t* table, int flags, uint64
   std::vector<int64_t> hseen(G);
   GD_CUDA(cudaMemcpyAsync(hs.data(), dsums.p, hs.size() * 8, cudaMemcpyDeviceToHost, s));
   GD_CUDA(cudaMemcpyAsync(hseen.data(), dseen.p, G * 8, cudaMemcpyDeviceToHost, s));
-  if (dtable.p && g.m)
-    GD_CUDA(cudaMemcpyAsync(table, dtable.p, (size_t)g.m * kNumMicro * 8, cudaMemcpyDeviceToHost,
-                            s));
+  if (dtable.p && g.m) copy_d2h(table, dtable.p, (size_t)g.m * kNumMicro * 8, s);
   GD_CUDA(cudaStreamSynchronize(s));
   store_timings(h, ex);
   ensure_pool_headroom(s);

@@ -423,8 +423,7 @@ void build_graph(DevGraph& g, const int64_t* pairs_in, int64_t k, int64_t n_decl
   const long long* dp = (const long long*)pairs_in;
   if (!(flags & GD_INPUT_DEVICE) && k) {
     pairs.alloc(2 * k, s);
-    GD_CUDA(cudaMemcpyAsync(pairs.p, pairs_in, 2 * k * sizeof(int64_t),
-                            cudaMemcpyHostToDevice, s));
+    copy_h2d(pairs.p, pairs_in, 2 * k * sizeof(int64_t), s);
     dp = pairs.p;
   }
 
@@ -539,8 +538,7 @@ void build_graph_batch(DevGraph& g, const int64_t* pairs_in, const int64_t* poff
   const long long* dp = (const long long*)pairs_in;
   if (!(flags & GD_INPUT_DEVICE) && k) {
     pairs.alloc(2 * k, s);
-    GD_CUDA(cudaMemcpyAsync(pairs.p, pairs_in, 2 * k * sizeof(int64_t),
-                            cudaMemcpyHostToDevice, s));
+    copy_h2d(pairs.p, pairs_in, 2 * k * sizeof(int64_t), s);
     dp = pairs.p;
   }
   DBuf<int64_t> d_poff, d_gn, d_voff;

@@ -161,6 +161,12 @@ T* ws_get(DevGraph&, const char* name, size_t count, cudaStream_t s) {
   return (T*)b.p;
 }
 
+// Host <-> device copies of caller buffers that may be pageable: large
+// pageable copies are staged through page-locked blocks by all host cores
+// (gd_copy.cu).  copy_d2h returns when the host buffer holds the data.
+void copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s);
+void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
+
 // ---------------------------------------------------------------------------
 // small device helpers
 // ---------------------------------------------------------------------------

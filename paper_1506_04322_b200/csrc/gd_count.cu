@@ -1877,10 +1877,12 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   const int64_t maxD = n ? dk.value(0) : 0;
   // graph-wide hit buffer (per-edge mode): exact-size lists for pass B.
   // Capacity = min(sum_a min(items_a, C(D_a, 2)) -- cached per graph --, 60% of
-  // the memory this process can still allocate (device free memory plus the
-  // unused reserve of the stream-ordered pool)).  The buffer lives for this
-  // census only (returned to the pool, so other censuses and builds can use
-  // it); if the allocation fails -- e.g. concurrent censuses on several host
+  // the memory this census can get: device free memory, the unused reserve
+  // of the stream-ordered pool and this thread's cached hit buffer).  The
+  // buffer is kept in the per-thread workspace (a fresh 76 GB stream-ordered
+  // allocation per census measured 0.4-0.8 s slower at config 5 once graph
+  // builds and tables interleave with it; gd_trim_workspace releases it).
+  // If the allocation fails -- e.g. concurrent censuses on several host
   // threads -- the capacity is halved, and at worst pass B re-probes every
   // frame (hit_cap = 0): slower, never wrong.
   const bool lists = env_int("GD_TRI_LISTS", 1) != 0;
@@ -1916,21 +1918,34 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
           res > used)
         spare = res - used;
     }
-    hit_cap = std::min<u64>(g.hit_cap, (u64)((fr + spare) * 0.6) / 8);
+    const auto it = thread_workspace().find("hitbuf");
+    const u64 mine = it != thread_workspace().end() ? (u64)it->second.bytes : 0;
+    hit_cap = std::min<u64>(g.hit_cap, (u64)((fr + spare + mine) * 0.6) / 8);
     hit_cap = std::min<u64>(hit_cap, (u64)env_int("GD_HIT_CAP", INT64_MAX));  // tests
+    const bool cached = env_int("GD_HIT_WS", 1) != 0;
     while (hit_cap) {
-      void* p = nullptr;
-      if (cudaMallocAsync(&p, hit_cap * 8, s) == cudaSuccess) {
-        hitbuf_mem.p = (u64*)p;
-        hitbuf_mem.n = hit_cap;
-        hitbuf_mem.s = s;
-        break;
+      if (cached) {
+        try {
+          hitbuf = ws_get<u64>(g, "hitbuf", hit_cap, s);
+          break;
+        } catch (const Error&) {
+          cudaGetLastError();
+          thread_workspace().erase("hitbuf");
+        }
+      } else {
+        void* p = nullptr;
+        if (cudaMallocAsync(&p, hit_cap * 8, s) == cudaSuccess) {
+          hitbuf_mem.p = (u64*)p;
+          hitbuf_mem.n = hit_cap;
+          hitbuf_mem.s = s;
+          hitbuf = hitbuf_mem.p;
+          break;
+        }
+        cudaGetLastError();  // out of memory: try half, then fall back to probing
       }
-      cudaGetLastError();  // out of memory: try half, then fall back to probing
       hit_cap = hit_cap > (1u << 20) ? hit_cap / 2 : 0;
     }
     if (hit_cap) {
-      hitbuf = hitbuf_mem.p;
       hittop = ws_get<u64>(g, "hittop", 1, s);
       GD_CUDA(cudaMemsetAsync(hittop, 0, 8, s));
       hoff = ws_get<int64_t>(g, "hoff", n, s);
@@ -2117,7 +2132,8 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   const int pe = per_edge ? 1 : 0;
   u64* c4s_p = per_edge ? c4s.p : nullptr;
   const int64_t nh = rh.second - rh.first;
-  int64_t n32 = 0, nrounds = 0;
+  int64_t n32 = 0, nrounds = 0, heavy_w = 0;
+  bool tiles_used = false;
   if (nh > 0) {
     std::vector<int> hf(nh);
     GD_CUDA(cudaMemcpyAsync(hf.data(), c4_frames.p + rh.first, nh * 4, cudaMemcpyDeviceToHost, s));
@@ -2133,6 +2149,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
         f16_all.push_back(hf[h]);
         w16_all.push_back((int64_t)(hkeys[h] >> 1));
         h16.push_back(h);
+        heavy_w += (int64_t)(hkeys[h] >> 1);
       }
     }
     n32 = (int64_t)f32_all.size();
@@ -2157,6 +2174,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     const int64_t max_tiles = (n - x0 + 90111) / 90112;
     const bool use_tiles = !force.c4_flow && !force.c4_cluster && tile_mode != 0 &&
                            (tile_mode == 2 || force.c4_tile64 || !per_edge || max_tiles <= 16);
+    tiles_used = use_tiles && !f16_all.empty();
     for (const int rk : my_ranks) {
     // this shard's frames: every world-th heavy frame in descending-work order
     std::vector<int> f16, f32;
@@ -2467,6 +2485,8 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     timer.mark("allreduce_bc");
   }
   stat("c4_coop_frames", nh - n32);
+  stat("c4_heavy_wedges", heavy_w);
+  stat("c4_tiles", tiles_used ? 1 : 0);
   stat("c4_rounds", nrounds);
   stat("c4_u32_hub_frames", n32);
   stat("c4_smem_frames", (rs0.second - rs0.first) + (rsa.second - rsa.first) +

@@ -17,7 +17,6 @@ from __future__ import annotations
 
 import ctypes
 import io
-import sys
 from pathlib import Path
 from typing import IO, Iterable
 
@@ -55,23 +54,6 @@ def _device_prefixes(options: ParseOptions):
     if len(enc) > 16:
         return None
     return enc
-
-
-_ASCII_OFFSET = sys.getsizeof("") - 1  # CPython: compact ASCII str data offset
-
-
-def _ascii_view(text: str):
-    """(address, length) of the bytes of an ASCII str without copying them
-    (CPython stores such strings as one byte per character right after the
-    object header); verified against the string, else None."""
-    if sys.implementation.name != "cpython" or not text.isascii():
-        return None
-    addr = id(text) + _ASCII_OFFSET
-    k = min(len(text), 64)
-    if ctypes.string_at(addr, k) != text[:k].encode("ascii") or \
-            ctypes.string_at(addr + len(text) - k, k) != text[len(text) - k:].encode("ascii"):
-        return None
-    return addr, len(text)
 
 
 def _parse_device(data, options: ParseOptions, cr_newline: bool, keep=None) -> Graph | None:
@@ -202,9 +184,7 @@ def load_edge_list(source: IO[str] | Iterable[str], options: ParseOptions | None
 def from_text(text: str, options: ParseOptions | None = None) -> Graph:
     """Graph.from_text (graph.py:164-166): lines split on '\\n' only."""
     options = options or ParseOptions()
-    view = _ascii_view(text)
-    if view is None and text.isascii():
-        view = text.encode("ascii")
+    view = text.encode("ascii") if text.isascii() else None
     g = _parse_device(view, options, cr_newline=False) if view is not None else None
     return g if g is not None else _load_lines(io.StringIO(text), options)
 

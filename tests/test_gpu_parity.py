@@ -261,3 +261,48 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def _mixed_hub_graph():
+    """K_{2,66000} (two frames whose counters may pass 16 bits: the u32 hub
+    path) plus a dense block (u16 heavy frames): the schedule mixes both
+    kinds of heavy frame, which a sharded census must deal out consistently."""
+    hubs = np.array([[0, 2 + i] for i in range(66000)] + [[1, 2 + i] for i in range(66000)],
+                    dtype=np.int64)
+    rng = np.random.default_rng(9)
+    base = 70000
+    iu = np.triu_indices(400, 1)
+    mask = rng.random(len(iu[0])) < 0.6
+    block = np.stack([iu[0][mask], iu[1][mask]], 1).astype(np.int64) + base
+    edges = np.concatenate([hubs, block])
+    return base + 400, edges
+
+
+@pytest.mark.parametrize("force", ["", "c4_coop", "c4_coop,c4_cluster", "c4_coop,c4_flow"])
+def test_sharded_mixed_u16_u32_heavy_frames(force):
+    """with u32 hub frames among the heavy frames, every shard
+    count must still see every u16 frame (cluster, flow and tile paths)."""
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import paper_1506_04322_b200 as gd
+from paper_1506_04322_b200.distributed import graphlet_census_sharded, micro_census_table_sharded
+from oracle import oracle as O
+import test_gpu_parity as T
+n, edges = T._mixed_hub_graph()
+g = gd.Graph(n, edges)
+tab, f = gd.micro_census_table(g)
+rows, sums = O.crosscheck_table(edges, n)
+assert np.array_equal(np.asarray(tab), rows)
+assert f.counts == O.close(sums, n, len(edges))
+assert gd.last_stats(g)["c4_u32_hub_frames"] >= 1
+for k in (2, 3):
+    assert graphlet_census_sharded(g, None, k) == f, k
+    t2, f2 = micro_census_table_sharded(g, None, k)
+    assert f2 == f and np.array_equal(np.asarray(t2), np.asarray(tab)), k
+print("ok")
+''' % (str(GOLDEN.parent.parent), str(GOLDEN.parent))
+    env = dict(os.environ, GD_FORCE_PATH=force)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

@@ -150,3 +150,28 @@ def test_library_closures_match_python_closures():
                 continue
             assert st[i] == 0, name
             assert counts_as_ints(out[i]) == [counts[c] for c in gd.CLASS_IDS], name
+
+
+def test_feature_matrix_skips_like_the_reference(monkeypatch):
+    """Batched feature_matrix records a failing graph as the reference does
+    (analytics.py:114-116: f"{type(exc).__name__}: {exc}" with the numbers)
+    and zips labels with graphs (a shorter label list drops graphs)."""
+    import numpy as np
+    import paper_1506_04322_b200.analytics as A
+
+    class FakeBatch:
+        num_graphs = 3
+        n_per_graph = np.array([5, 5, 5])
+        m_per_graph = np.array([1, 1, 1])
+
+    monkeypatch.setattr(A.GraphBatch, "from_graphs", staticmethod(lambda gs: FakeBatch()))
+    sums = np.zeros((3, 26), np.uint64)
+    sums[1, 0] = 4  # triangle sum 4: not divisible by 3
+    counts = np.zeros((3, 17, 2), np.int64)
+    status = np.array([0, 1, 0], dtype=np.int32)
+    monkeypatch.setattr(A, "batch_counts", lambda b, with_sums=False: (counts, status, sums))
+    fm = A.feature_matrix([object(), object(), object()], labels=["a", "b", "c"])
+    assert fm.skipped == [("b", "ConsistencyError: triangle closure: 4 not divisible by 3")]
+    assert fm.labels == ["a", "c"]
+    fm = A.feature_matrix([object(), object(), object()], labels=["a", "b"])
+    assert fm.labels == ["a"] and len(fm.skipped) == 1

@@ -2,7 +2,7 @@
 as in bench.py's e2e leg): build from pinned host pairs, census into a device
 table (first and second census of the graph), D2H of the table."""
 import sys, time
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parent.parent))
 import numpy as np
 import torch
 import paper_1506_04322_b200 as gd

@@ -1,7 +1,7 @@
 """Step-by-step timing of the e2e path (fresh graph per step) with device
 memory use, to find allocation / synchronisation spikes."""
 import sys, time, gc
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parent.parent))
 import numpy as np, torch
 import paper_1506_04322_b200 as gd
 from paper_1506_04322_b200 import _native as N, workloads as W

@@ -1,6 +1,6 @@
 """One warm per-edge (or global) census of a config, for ncu captures."""
 import sys
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parent.parent))
 import paper_1506_04322_b200 as gd
 from paper_1506_04322_b200 import _native as N
 from paper_1506_04322_b200 import workloads as W

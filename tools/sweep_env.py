@@ -6,7 +6,7 @@ vals = sys.argv[3].split(",")
 mode = sys.argv[4] if len(sys.argv) > 4 else "per_edge"
 code = r'''
 import sys, json
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, %r)
 import paper_1506_04322_b200 as gd
 from paper_1506_04322_b200 import _native as N, workloads as W
 raw = W.config_graph(%r)
@@ -22,7 +22,7 @@ for i in range(4):
         if i == 0: print("check failed (expected under GD_EXP):", exc)
     if i: res.append(gd.last_timings(g))
 print(json.dumps(res[-1]), sum(sum(r.values()) for r in res) / len(res))
-''' % (cfg, mode)
+''' % (str(__import__('pathlib').Path(__file__).resolve().parent.parent), cfg, mode)
 for v in vals:
     env = dict(os.environ, **{var: v})
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)

@@ -1,5 +1,5 @@
 import sys, time
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parent.parent))
 import numpy as np
 import paper_1506_04322_b200 as gd
 from paper_1506_04322_b200 import workloads as W

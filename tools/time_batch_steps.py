@@ -1,7 +1,7 @@
 """Where the config-4 feature_matrix e2e time goes (host packing, device
 build, census + closures, row assembly)."""
 import sys, time
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parent.parent))
 import numpy as np
 import paper_1506_04322_b200 as gd
 from paper_1506_04322_b200 import workloads as W

@@ -5,7 +5,7 @@ import io
 import json
 import sys
 import time
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parent.parent))
 import numpy as np
 import paper_1506_04322_b200 as gd
 from paper_1506_04322_b200 import edgelist as EL, workloads as W
