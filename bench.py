@@ -334,9 +334,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             from paper_1506_04322_b200.distributed import (graphlet_census_sharded,
                                                            micro_census_table_sharded)
             if per_edge:
+                # this rank's rows (shard_rows) of the table
                 t, f = micro_census_table_sharded(graph, comm, device_out=device_out)
                 if out is not None:
-                    out[...] = t
+                    from paper_1506_04322_b200.distributed import shard_rows
+                    e0, e1 = shard_rows(graph.m, comm.rank, comm.world)
+                    out[e0:e1] = t
                 return f
             return graphlet_census_sharded(graph, comm)
         if per_edge:
@@ -460,7 +463,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "dtype": "int64", "data": "synthetic",
             "config": {"workload": args.config, "mode": args.mode,
                        "graph": CONFIG_DESC[args.config], "n": n, "m": m,
-                       "parallelism": f"frame-sharded x{world} (NCCL all-reduce)" if world > 1
+                       "parallelism": f"frame-sharded x{world}, owned edge ranges (NCCL "
+                                      "all-reduce + reduce-scatter)" if world > 1
                        else "single",
                        "l2": "flushed between steps (256 MiB device memset)",
                        "timing": "CUDA events on the library stream, whole census"},

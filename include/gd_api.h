@@ -147,13 +147,19 @@ GD_API int gd_census_per_edge_edges(const int64_t* edges, int64_t m, int64_t n, 
                              int64_t* table, uint64_t* sums, int64_t* edges_seen);
 
 /*
- * Multi-GPU (one process per GPU).  gd_comm_unique_id on rank 0 (128 bytes,
- * broadcast by the caller), gd_comm_init on every rank (NCCL is loaded at
- * this point).  gd_census_sharded deals the frames of the counting passes
- * round-robin to the ranks and sums the per-slot partial counters with NCCL
- * all-reduce between passes (the reference's fixed-order merge of worker
- * accumulators, parallel.py:138-143); every rank returns the full result.
- * comm == NULL with virtual_ranks = K emulates K shards on this GPU.
+ * Multi-GPU (one process per GPU; replaces the worker pool of run_batches,
+ * parallel.py:85-149).  gd_comm_unique_id on rank 0 (128 bytes, broadcast by
+ * the caller), gd_comm_init on every rank (NCCL is loaded at this point).
+ * gd_census_sharded deals the frames of the counting passes round-robin to
+ * the ranks; each rank owns the contiguous canonical edge range
+ * gd_shard_rows(m, rank, world).  Between the passes the
+ * per-edge triangle counters are all-reduced and the per-edge partial sums
+ * reduce-scattered onto their owners; each rank finalizes -- and writes to
+ * `table` -- only its own rows (e1 - e0 rows), and every rank returns the
+ * global 13 sums (128-bit, all-gathered and added exactly; the reference's
+ * fixed-order merge of worker accumulators, parallel.py:138-143).
+ * comm == NULL with virtual_ranks = K emulates K shards on this GPU (their
+ * ranges together: the full table).
  */
 typedef struct gd_comm gd_comm;
 GD_API int gd_comm_unique_id(unsigned char* id_out);
@@ -161,6 +167,7 @@ GD_API int gd_comm_init(const unsigned char* id, int rank, int world, gd_comm** 
 GD_API void gd_comm_free(gd_comm* comm);
 GD_API int gd_census_sharded(gd_graph* g, gd_comm* comm, int virtual_ranks, int per_edge,
                              int64_t* table, int flags, uint64_t* sums, int64_t* edges_seen);
+GD_API int gd_shard_rows(int64_t m, int rank, int world, int64_t* e0, int64_t* e1);
 
 /*
  * Device timings (CUDA events on the library stream) of the phases of the

@@ -62,6 +62,7 @@ SIGNATURES = (
     ("gd_comm_free", None, [_vp]),
     ("gd_census_sharded", ctypes.c_int, [_vp, _vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int,
                                          _u64p, _i64p]),
+    ("gd_shard_rows", ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int, _i64p, _i64p]),
     ("gd_close_counts", ctypes.c_int, [_u64p, _i64p, _i64p, ctypes.c_int64, _i64p,
                                        ctypes.POINTER(ctypes.c_int)]),
     ("gd_set_device", ctypes.c_int, [ctypes.c_int]),

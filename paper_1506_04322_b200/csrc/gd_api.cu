@@ -38,6 +38,8 @@ struct NcclApi {
                             cudaStream_t);
   ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t);
+  ncclResult_t (*reduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                                ncclComm_t, cudaStream_t);
   ncclResult_t (*commDestroy)(ncclComm_t);
   const char* (*getErrorString)(ncclResult_t);
 };
@@ -66,10 +68,12 @@ static const NcclApi& nccl() {
     api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
     api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
     api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+    api.reduceScatter = (decltype(api.reduceScatter))dlsym(h, "ncclReduceScatter");
     api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
     api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
   });
-  if (!api.allReduce) throw Error(GD_ECUDA, err.empty() ? "NCCL symbols missing" : err);
+  if (!api.allReduce || !api.reduceScatter)
+    throw Error(GD_ECUDA, err.empty() ? "NCCL symbols missing" : err);
   return api;
 }
 
@@ -248,21 +252,26 @@ static void census(gd_graph* h, bool per_edge, int64_t* table, int flags, uint64
   dseen.alloc(G, s);
   DBuf<long long> dtable;
   long long* tptr = nullptr;
+  // a real multi-GPU census writes only this rank's rows (shard_rows)
+  int64_t r0 = 0, r1 = g.m;
+  if (shard.real() && G == 1) shard_rows(g.m, shard.rank, shard.world, &r0, &r1);
   if (per_edge && table) {
     if (flags & GD_OUTPUT_DEVICE) {
       tptr = (long long*)table;
     } else {
-      dtable.alloc((size_t)g.m * kNumMicro, s);
+      dtable.alloc((size_t)std::max<int64_t>(r1 - r0, 1) * kNumMicro, s);
       tptr = dtable.p;
     }
   }
   CensusExtras ex;
   run_census(g, per_edge, tptr, dsums.p, dseen.p, ex, s, shard);
+  if (ex.rows >= 0 && (ex.row0 != r0 || ex.rows != r1 - r0))
+    throw Error(GD_ECUDA, "shard row range mismatch");
   std::vector<uint64_t> hs(G * 2 * kNumSums);
   std::vector<int64_t> hseen(G);
   GD_CUDA(cudaMemcpyAsync(hs.data(), dsums.p, hs.size() * 8, cudaMemcpyDeviceToHost, s));
   GD_CUDA(cudaMemcpyAsync(hseen.data(), dseen.p, G * 8, cudaMemcpyDeviceToHost, s));
-  if (dtable.p && g.m) copy_d2h(table, dtable.p, (size_t)g.m * kNumMicro * 8, s);
+  if (dtable.p && r1 > r0) copy_d2h(table, dtable.p, (size_t)(r1 - r0) * kNumMicro * 8, s);
   GD_CUDA(cudaStreamSynchronize(s));
   store_timings(h, ex);
   ensure_pool_headroom(s);
@@ -504,11 +513,24 @@ int gd_census_sharded(gd_graph* h, gd_comm* c, int virtual_ranks, int per_edge, 
                                size_t count) {
         GD_NCCL(nccl().allGather(in, out, count, ncclUint64, comm, s));
       };
+      sh.reduce_scatter = [s, comm](const void* in, void* out, size_t count, int esz) {
+        GD_NCCL(nccl().reduceScatter(in, out, count, esz == 4 ? ncclUint32 : ncclUint64,
+                                     ncclSum, comm, s));
+      };
     } else {
       sh.world = virtual_ranks;
     }
     census(h, per_edge != 0, table, flags, sums, edges_seen, sh);
   });
+}
+
+int gd_shard_rows(int64_t m, int rank, int world, int64_t* e0, int64_t* e1) {
+  if (!e0 || !e1 || world < 1 || rank < 0 || rank >= world || m < 0) {
+    t_last_error = "bad shard arguments";
+    return GD_EINVAL;
+  }
+  shard_rows(m, rank, world, e0, e1);
+  return GD_OK;
 }
 
 // Closures of census.py:388-430 in exact 128-bit integers, for many graphs

@@ -1543,27 +1543,99 @@ __device__ __forceinline__ void store_row(long long* __restrict__ table, int64_t
   }
 }
 
-// G == 1: grid-stride over edges
+// G == 1: grid-stride over the edges [e0, e1); row e is written at table
+// row e - e0 (a rank's shard of the table in a multi-GPU census)
 template <int NT>
 __global__ void __launch_bounds__(NT)
-k_finalize_single(EdgeIn in, int64_t m_edges, long long n, long long m,
+k_finalize_single(EdgeIn in, int64_t e0, int64_t e1, long long n, long long m,
                   long long* __restrict__ table, u64* __restrict__ sums, u64* __restrict__ seen) {
   u128 acc[kNumSums];
   for (int k = 0; k < kNumSums; k++) acc[k] = 0;
   u64 cnt = 0;
   long long row[kNumMicro];
-  for (int64_t e = blockIdx.x * (int64_t)NT + threadIdx.x; e < m_edges;
+  for (int64_t e = e0 + blockIdx.x * (int64_t)NT + threadIdx.x; e < e1;
        e += (int64_t)gridDim.x * NT) {
     edge_row(in, e, row);
     add_sums(acc, row[0], row[1], row[2], row[3], in.tsl ? row[4] : 0, n, m);
     cnt++;
-    if (table) store_row(table, e, row);
+    if (table) store_row(table, e - e0, row);
   }
   block_flush_sums<NT>(acc, sums);
   typedef cub::BlockReduce<u64, NT> BR;
   __shared__ typename BR::TempStorage tmp2;
   const u64 c = BR(tmp2).Sum(cnt);
   if (threadIdx.x == 0 && c) atomicAdd(seen, c);
+}
+
+// ---- multi-GPU ownership (gd_count.cuh: Shard) ----------------------------
+// per-edge partials of passes B and C in rank-major blocks [W][4][M]: the
+// block of rank r holds the 4 fields of its owned edges [r*M, (r+1)*M)
+template <typename ST>
+__global__ void k_pack_edge_partials(int64_t m, int64_t M, const int64_t* __restrict__ e2o,
+                                     const int64_t* __restrict__ e2i, const ST* __restrict__ tsl,
+                                     const ST* __restrict__ tsh, const ST* __restrict__ tsd,
+                                     const ST* __restrict__ c4s, ST* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / M, i = e - r * M, q = e2o[e];
+    ST* b = out + r * 4 * M;
+    b[i] = tsl[q];
+    b[M + i] = tsh[q];
+    b[2 * M + i] = tsd[q];
+    b[3 * M + i] = c4s[q] + c4s[e2i[e]];
+  }
+}
+
+// an owner's reduced block back into the slot-indexed arrays the finalize reads
+template <typename ST>
+__global__ void k_unpack_owned(int64_t e0, int64_t e1, int64_t M, const int64_t* __restrict__ e2o,
+                               const int64_t* __restrict__ e2i, const ST* __restrict__ in,
+                               ST* __restrict__ tsl, ST* __restrict__ tsh, ST* __restrict__ tsd,
+                               ST* __restrict__ c4s) {
+  for (int64_t e = e0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < e1;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e - e0, q = e2o[e];
+    tsl[q] = in[i];
+    tsh[q] = in[M + i];
+    tsd[q] = in[2 * M + i];
+    c4s[q] = in[3 * M + i];
+    c4s[e2i[e]] = 0;
+  }
+}
+
+// pass-A counters: slot-indexed (out-slots only) <-> edge-indexed
+__global__ void k_gather_edges(int64_t m, const int64_t* __restrict__ e2o,
+                               const u64* __restrict__ slots, u64* __restrict__ edges) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x)
+    edges[e] = slots[e2o[e]];
+}
+
+__global__ void k_scatter_edges(int64_t m, const int64_t* __restrict__ e2o,
+                                const u64* __restrict__ edges, u64* __restrict__ slots) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x)
+    slots[e2o[e]] = edges[e];
+}
+
+// 128-bit sums and edge counts of every rank (all-gathered) added exactly
+__global__ void k_sum_shards(const u64* __restrict__ gsums, const u64* __restrict__ gseen, int W,
+                             u64* __restrict__ sums, u64* __restrict__ seen) {
+  const int k = threadIdx.x;
+  if (k < kNumSums) {
+    u128 t = 0;
+    for (int r = 0; r < W; r++) {
+      const u64* p = gsums + (size_t)r * 2 * kNumSums + 2 * k;
+      t += ((u128)p[1] << 64) | p[0];
+    }
+    sums[2 * k] = (u64)t;
+    sums[2 * k + 1] = (u64)(t >> 64);
+  }
+  if (k == 0) {
+    u64 c = 0;
+    for (int r = 0; r < W; r++) c += gseen[r];
+    *seen = c;
+  }
 }
 
 // G > 1: one CTA per graph
@@ -1831,7 +1903,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   // edge e = (u, v): C4(e) <= (d(u)-1)(d(v)-1), sum_{w in Tri_e} t(lo, w) and
   // sum d(w) <= (dmax-1) dmax < 2^32), halving the sectors of their coalesced
   // atomics; u64 otherwise and for real shards (64-bit NCCL sums)
-  const bool narrow = per_edge && !sh.real() && g.max_deg < 65536 &&
+  const bool narrow = per_edge && g.max_deg < 65536 &&
                       env_int("GD_WIDE_SLOTS", 0) == 0;
   const size_t slot_words = narrow ? (S + 1) / 2 : S;
   WBuf tsl{nullptr}, tsh{nullptr}, tsd{nullptr}, c4s{nullptr};
@@ -2097,7 +2169,20 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   };
   run_frames(false);
   timer.mark("tri_frames");
-  if (sh.real()) {  // per-slot triangle / 4-clique counts and T(x) of all shards
+  // multi-GPU ownership (gd_count.cuh): G == 1 graphs split their rows
+  const bool owned = (world > 1 || sh.real()) && G == 1 && m > 0;
+  if (owned) {  // t / cl of every edge and T(x): all ranks need them in pass B
+    u64* tce = ws_get<u64>(g, "tce", (size_t)m, s);
+    k_gather_edges<<<grid_cap(m, 256), 256, 0, s>>>(m, g.e2o.p, tcs.p, tce);
+    GD_LAUNCH_CHECK("gather_edges");
+    if (sh.real()) {
+      sh.allreduce(tce, (size_t)m);
+      sh.allreduce(vT.p, (size_t)n);
+    }
+    k_scatter_edges<<<grid_cap(m, 256), 256, 0, s>>>(m, g.e2o.p, tce, tcs.p);
+    GD_LAUNCH_CHECK("scatter_edges");
+    timer.mark("allreduce_a");
+  } else if (sh.real()) {  // batches: every slot of every shard
     sh.allreduce(tcs.p, (size_t)S);
     sh.allreduce(vT.p, (size_t)n);
     timer.mark("allreduce_a");
@@ -2477,7 +2562,33 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   smem_bin(rs0, GD_SMK(64, false), 64, false, 32);
 #undef GD_SMK
   timer.mark("c4_smem");
-  if (sh.real() && per_edge) {  // per-slot triangle sums and 4-cycle counts of all shards
+  // owned edge ranges: per-edge partials reduce-scattered onto their owners
+  const int64_t M = owned ? (m + world - 1) / world : m;
+  if (owned && per_edge) {
+    const int esz = narrow ? 4 : 8;
+    char* packed = ws_get<char>(g, "packed", (size_t)world * 4 * M * esz, s);
+    char* mine = ws_get<char>(g, "owned", (size_t)4 * M * esz, s);
+#define GD_PACK(ST)                                                                               \
+    k_pack_edge_partials<ST><<<grid_cap(m, 256), 256, 0, s>>>(m, M, g.e2o.p, g.e2i.p, (ST*)tsl.p, \
+        (ST*)tsh.p, (ST*)tsd.p, (ST*)c4s.p, (ST*)packed)
+    if (narrow) GD_PACK(unsigned); else GD_PACK(u64);
+#undef GD_PACK
+    GD_LAUNCH_CHECK("pack_edge_partials");
+    if (sh.real()) sh.reduce_scatter(packed, mine, (size_t)4 * M, esz);
+    for (const int rk : my_ranks) {
+      int64_t e0, e1;
+      shard_rows(m, rk, world, &e0, &e1);
+      if (e1 <= e0) continue;
+      const char* src = sh.real() ? mine : packed + (size_t)rk * 4 * M * esz;
+#define GD_UNPACK(ST)                                                                             \
+      k_unpack_owned<ST><<<grid_cap(e1 - e0, 256), 256, 0, s>>>(e0, e1, M, g.e2o.p, g.e2i.p,       \
+          (const ST*)src, (ST*)tsl.p, (ST*)tsh.p, (ST*)tsd.p, (ST*)c4s.p)
+      if (narrow) GD_UNPACK(unsigned); else GD_UNPACK(u64);
+#undef GD_UNPACK
+      GD_LAUNCH_CHECK("unpack_owned");
+    }
+    timer.mark("reduce_scatter_bc");
+  } else if (sh.real() && per_edge) {  // batches: every slot of every shard
     sh.allreduce(tsl.p, (size_t)S);
     sh.allreduce(tsh.p, (size_t)S);
     sh.allreduce(tsd.p, (size_t)S);
@@ -2511,9 +2622,34 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   in.vS = vS.p;
   GD_CUDA(cudaMemsetAsync(sums_dev, 0, (size_t)G * 2 * kNumSums * 8, s));
   GD_CUDA(cudaMemsetAsync(seen_dev, 0, (size_t)G * 8, s));
-  if (G == 1) {
+  if (G == 1 && owned) {
+    // real: this rank's rows into its table shard, then all ranks' sums
+    // added; emulated: every rank's range at its offset of the full table
+    for (const int rk : my_ranks) {
+      int64_t e0, e1;
+      shard_rows(m, rk, world, &e0, &e1);
+      if (rk == sh.rank || !sh.real()) {
+        ex.row0 = sh.real() ? e0 : 0;
+        ex.rows = sh.real() ? e1 - e0 : m;
+      }
+      if (e1 <= e0) continue;
+      long long* tp = table_dev ? table_dev + (sh.real() ? 0 : e0 * kNumMicro) : nullptr;
+      k_finalize_single<256><<<grid_cap(e1 - e0, 256, 4), 256, 0, s>>>(in, e0, e1, n, m, tp,
+                                                                       sums_dev, seen_dev);
+      GD_LAUNCH_CHECK("finalize_single");
+    }
+    if (sh.real()) {
+      DBuf<u64> gs, gn;
+      gs.alloc((size_t)world * 2 * kNumSums, s);
+      gn.alloc((size_t)world, s);
+      sh.allgather(sums_dev, gs.p, (size_t)(2 * kNumSums));
+      sh.allgather(seen_dev, gn.p, 1);
+      k_sum_shards<<<1, 32, 0, s>>>(gs.p, gn.p, world, sums_dev, seen_dev);
+      GD_LAUNCH_CHECK("sum_shards");
+    }
+  } else if (G == 1) {
     if (m) {
-      k_finalize_single<256><<<grid_cap(m, 256, 4), 256, 0, s>>>(in, m, n, m, table_dev,
+      k_finalize_single<256><<<grid_cap(m, 256, 4), 256, 0, s>>>(in, 0, m, n, m, table_dev,
                                                                  sums_dev, seen_dev);
       GD_LAUNCH_CHECK("finalize_single");
     }

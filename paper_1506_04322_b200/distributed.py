@@ -2,11 +2,17 @@
 
 Single large graph: ``CensusComm`` wraps the library's NCCL communicator
 (gd_comm_*); ``graphlet_census_sharded`` / ``micro_census_table_sharded``
-deal the counting frames round-robin to the ranks and sum the per-slot
-partial counters with NCCL all-reduce between the passes (the reference's
-fixed-order merge of worker accumulators, parallel.py:138-143).  Every rank
-returns the full result.  ``virtual_ranks=K`` without a communicator emulates
-K shards on one GPU (the single-GPU check of the partitioning).
+deal the counting frames round-robin to the ranks.  Each rank owns the
+contiguous canonical edge range ``shard_rows(m, rank, world)`` (SURVEY
+8(e)): the per-edge triangle counters are all-reduced after pass A, the
+per-edge partial sums of passes B and C are reduce-scattered onto their
+owners, every rank finalizes only its rows, and the 128-bit totals are
+all-gathered and added (the reference's fixed-order merge of worker
+accumulators, parallel.py:138-143).  Every rank returns the global counts
+and its own block of the per-edge table (``gather_table`` assembles the
+whole table where it is wanted).  ``virtual_ranks=K`` without a
+communicator emulates K shards on one GPU (the single-GPU check of the
+partition: the packing, ownership and per-range finalize all run).
 
 Many small graphs (config 4): ``feature_matrix_distributed`` shards the
 graphs by rank (contiguous, balanced by edge count) with no data-path
@@ -74,18 +80,47 @@ def graphlet_census_sharded(g, comm: CensusComm | None = None, virtual_ranks: in
     return _sharded(g, comm, virtual_ranks, False, None, 0)
 
 
+def shard_rows(m: int, rank: int, world: int) -> tuple[int, int]:
+    """Owned canonical edge range [e0, e1) of ``rank``: blocks of
+    ceil(m / world) edges (the library's gd_shard_rows)."""
+    M = -(-int(m) // world) if world > 0 else int(m)
+    e0 = min(int(m), rank * M)
+    return e0, min(int(m), e0 + M)
+
+
 def micro_census_table_sharded(g, comm: CensusComm | None = None, virtual_ranks: int = 1,
                                device_out: int | None = None):
-    """micro_census_table with the frames split over the ranks of ``comm``
-    (every rank finalizes, and receives, the whole table)."""
+    """micro_census_table with the frames split over the ranks of ``comm``.
+    With a communicator the returned table holds this rank's rows
+    ``shard_rows(m, comm.rank, comm.world)``; emulated (``virtual_ranks``)
+    it is the whole table."""
     m = int(g.m)
     if m == 0:
         return np.zeros((0, N.NUM_MICRO), np.int64), frequencies_from_sums(CensusSums(), int(g.n), 0)
     if device_out is not None:
         return None, _sharded(g, comm, virtual_ranks, True, ctypes.c_void_p(int(device_out)),
                               N.GD_OUTPUT_DEVICE)
-    table = N.pinned_empty((m, N.NUM_MICRO))
+    e0, e1 = shard_rows(m, comm.rank, comm.world) if comm is not None else (0, m)
+    table = N.pinned_empty((e1 - e0, N.NUM_MICRO))
     return table, _sharded(g, comm, virtual_ranks, True, N.vptr(table), 0)
+
+
+def gather_table(block: np.ndarray, m: int, group=None) -> np.ndarray:
+    """The whole (m, 10) table on every rank from the ranks' owned blocks
+    (torch.distributed all-gather of the row blocks, in rank order)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    M = -(-int(m) // world)
+    pad = np.zeros((M, N.NUM_MICRO), dtype=np.int64)
+    pad[:len(block)] = block
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else \
+        torch.device("cpu")
+    mine = torch.from_numpy(pad).to(dev)
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine, group=group)
+    return torch.cat(parts).cpu().numpy()[:int(m)]
 
 
 def shard_bounds(weights, world: int) -> list[int]:
