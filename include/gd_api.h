@@ -83,6 +83,15 @@ GD_API int gd_graph_create(const int64_t* pairs, int64_t k, int64_t n, int ids_m
 GD_API int gd_graph_create_batch(const int64_t* pairs, const int64_t* pair_offsets,
                           const int64_t* n_per_graph, int64_t num_graphs,
                           int flags, gd_graph** out);
+/*
+ * The same from one int64 [k_g][2] array per graph (pair_lists[g], k_g =
+ * pair_offsets[g+1] - pair_offsets[g]): the library gathers them into
+ * page-locked staging with all host cores, so callers holding a list of
+ * per-graph arrays (feature_matrix's `graphs`) need no packing pass.
+ */
+GD_API int gd_graph_create_batch_list(const int64_t* const* pair_lists,
+                                      const int64_t* pair_offsets, const int64_t* n_per_graph,
+                                      int64_t num_graphs, int flags, gd_graph** out);
 
 /* n, m and number of graphs of a device graph (batched: totals) */
 GD_API int gd_graph_info(const gd_graph* g, int64_t* n, int64_t* m, int64_t* num_graphs);

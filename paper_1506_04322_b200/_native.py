@@ -40,6 +40,8 @@ SIGNATURES = (
                                        ctypes.c_int, ctypes.POINTER(_vp)]),
     ("gd_graph_create_batch", ctypes.c_int, [_vp, _i64p, _i64p, ctypes.c_int64, ctypes.c_int,
                                              ctypes.POINTER(_vp)]),
+    ("gd_graph_create_batch_list", ctypes.c_int, [_vp, _i64p, _i64p, ctypes.c_int64,
+                                                  ctypes.c_int, ctypes.POINTER(_vp)]),
     ("gd_graph_info", ctypes.c_int, [_vp, _i64p, _i64p, _i64p]),
     ("gd_graph_sizes", ctypes.c_int, [_vp, _i64p, _i64p]),
     ("gd_graph_export", ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),

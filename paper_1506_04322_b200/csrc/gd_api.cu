@@ -275,7 +275,7 @@ static void census(gd_graph* h, bool per_edge, int64_t* table, int flags, uint64
   GD_CUDA(cudaStreamSynchronize(s));
   store_timings(h, ex);
   ensure_pool_headroom(s);
-  close_cycles(hs.data(), ex, G, per_edge);
+  if (!ex.direct) close_cycles(hs.data(), ex, G, per_edge);
   if (sums) std::memcpy(sums, hs.data(), hs.size() * 8);
   if (seen) std::memcpy(seen, hseen.data(), G * 8);
 }
@@ -331,6 +331,33 @@ int gd_graph_create_batch(const int64_t* pairs, const int64_t* pair_offsets,
   int rc = guarded([&] {
     h->s = acquire_stream();
     build_graph_batch(h->g, pairs, pair_offsets, n_per_graph, num_graphs, flags, h->s);
+  });
+  if (rc != GD_OK) {
+    gd_graph_free(h);
+    return rc;
+  }
+  *out = h;
+  return GD_OK;
+}
+
+int gd_graph_create_batch_list(const int64_t* const* lists, const int64_t* pair_offsets,
+                               const int64_t* n_per_graph, int64_t num_graphs, int flags,
+                               gd_graph** out) {
+  if (!out || !pair_offsets || !n_per_graph || (num_graphs > 0 && !lists)) {
+    t_last_error = "NULL argument";
+    return GD_EINVAL;
+  }
+  *out = nullptr;
+  gd_graph* h = new gd_graph();
+  int rc = guarded([&] {
+    h->s = acquire_stream();
+    const int64_t k = num_graphs > 0 ? pair_offsets[num_graphs] - pair_offsets[0] : 0;
+    if (k < 0 || (num_graphs > 0 && pair_offsets[0] != 0))
+      throw Error(GD_EINVAL, "bad pair_offsets");
+    int64_t* flat = (int64_t*)host_staging((size_t)std::max<int64_t>(k, 1) * 16);
+    gather_pairs(lists, pair_offsets, num_graphs, flat);
+    build_graph_batch(h->g, flat, pair_offsets, n_per_graph, num_graphs, flags & ~GD_INPUT_DEVICE,
+                      h->s);
   });
   if (rc != GD_OK) {
     gd_graph_free(h);

@@ -166,6 +166,11 @@ T* ws_get(DevGraph&, const char* name, size_t count, cudaStream_t s) {
 // (gd_copy.cu).  copy_d2h returns when the host buffer holds the data.
 void copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s);
 void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
+// This thread's page-locked host staging block of at least `bytes` (grown,
+// never shrunk; valid until the next call on the same thread), and the
+// parallel gather of per-graph pair arrays into it.
+void* host_staging(size_t bytes);
+void gather_pairs(const int64_t* const* lists, const int64_t* offs, int64_t G, int64_t* flat);
 
 // ---------------------------------------------------------------------------
 // small device helpers

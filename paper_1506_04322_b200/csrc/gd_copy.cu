@@ -113,4 +113,33 @@ void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   for (size_t c = nchunks > (size_t)kSlots ? nchunks - kSlots : 0; c < nchunks; c++) drain(c);
 }
 
+void* host_staging(size_t bytes) {
+  struct Block {
+    void* p = nullptr;
+    size_t n = 0;
+    ~Block() {
+      if (p) cudaFreeHost(p);
+    }
+  };
+  static thread_local Block b;
+  if (b.n < bytes) {
+    const size_t want = std::max(bytes, b.n * 2);
+    if (b.p) cudaFreeHost(b.p);
+    b.p = nullptr;
+    b.n = 0;
+    GD_CUDA(cudaHostAlloc(&b.p, want, cudaHostAllocDefault));
+    b.n = want;
+  }
+  return b.p;
+}
+
+void gather_pairs(const int64_t* const* lists, const int64_t* offs, int64_t G, int64_t* flat) {
+  const int nt = std::min(8, std::max(1, omp_get_max_threads()));
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 64)
+  for (int64_t g = 0; g < G; g++) {
+    const int64_t k = offs[g + 1] - offs[g];
+    if (k > 0) std::memcpy(flat + 2 * offs[g], lists[g], (size_t)k * 16);
+  }
+}
+
 }  // namespace gd

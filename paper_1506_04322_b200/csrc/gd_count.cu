@@ -1567,6 +1567,240 @@ k_finalize_single(EdgeIn in, int64_t e0, int64_t e1, long long n, long long m,
   if (threadIdx.x == 0 && c) atomicAdd(seen, c);
 }
 
+// ---- small graphs: the reference's marks protocol, one kernel ------------
+// Graphs (or batches of graphs) whose adjacency fits in shared memory are
+// counted by a direct restatement of _micro_edge (census.py:190-256) on the
+// device: the CTA stages its graph's CSR in local dense ids, each warp takes
+// edges and keeps a private n-byte marks array (1 = N(u) only, 2 = Tri,
+// 3 = N(v) only), and the ten per-edge fields and 13 sums come out of one
+// launch -- no schedule, no passes, no host round trips (config 1: 10,000
+// edges; config 4: 4,096 graphs, one CTA each).
+struct SmallIn {
+  const int64_t* rp;    // rank CSR
+  const int32_t* col;
+  const int32_t* eu;    // canonical edges (dense ids)
+  const int32_t* ev;
+  const int32_t* d2r;
+  const int32_t* r2d;
+  const int64_t* voff;  // [G+1] dense vertex offset of each graph
+  const int64_t* eoff;  // [G+1] canonical edge offset of each graph
+};
+
+// 2-bit marks, private to one thread, laid out word-major / lane-minor so the
+// 32 lanes of a warp always hit 32 different banks
+struct LaneMarks {
+  unsigned* w;  // word i of this thread at w[i * NT]
+  int stride;
+  __device__ __forceinline__ unsigned get(int x) const {
+    return (w[(x >> 4) * stride] >> ((x & 15) << 1)) & 3u;
+  }
+  __device__ __forceinline__ void set(int x, unsigned v) const {
+    unsigned* p = w + (x >> 4) * stride;
+    const int sh = (x & 15) << 1;
+    *p = (*p & ~(3u << sh)) | (v << sh);
+  }
+};
+
+// Adjacency of a small-graph census: rank-space rows in global memory (one
+// graph) or local dense rows staged in shared memory (a batch, whose
+// graphs' vertices are scattered over the rank space).
+struct GlobalRows {
+  const int64_t* rp;
+  const int32_t* col;
+  __device__ __forceinline__ int deg(int x) const { return (int)(rp[x + 1] - rp[x]); }
+  __device__ __forceinline__ const int32_t* row(int x) const { return col + rp[x]; }
+};
+struct SharedRows {
+  const int* off;
+  const int* adj;
+  __device__ __forceinline__ int deg(int x) const { return off[x + 1] - off[x]; }
+  __device__ __forceinline__ const int* row(int x) const { return adj + off[x]; }
+};
+
+template <int NT, bool BATCH>
+__global__ void __launch_bounds__(NT)
+k_small_census(SmallIn in, int G, int words, long long* __restrict__ table,
+               u64* __restrict__ sums, u64* __restrict__ seen) {
+  extern __shared__ __align__(16) int sm_i[];
+  const int gi = BATCH ? blockIdx.x : 0;
+  const int64_t v0 = in.voff[gi], e0 = in.eoff[gi], e1 = in.eoff[gi + 1];
+  const int nv = (int)(in.voff[gi + 1] - v0);
+  unsigned* marks = (unsigned*)sm_i;  // [words][NT]
+  for (int i = threadIdx.x; i < words * NT; i += NT) marks[i] = 0u;
+  typename std::conditional<BATCH, SharedRows, GlobalRows>::type R;
+  if constexpr (BATCH) {
+    // stage the graph in local dense ids: degrees, offsets (block scan),
+    // rows (thread per vertex, its row converted rank -> local dense)
+    int* off = (int*)(marks + (size_t)words * NT);  // [nv + 1]
+    int* adj = off + nv + 1;                        // [2 m_g]
+    typedef cub::BlockScan<int, NT> BS;
+    __shared__ typename BS::TempStorage scan_tmp;
+    const int per = (nv + NT - 1) / NT;
+    int local = 0;
+    int64_t rb[8];
+    for (int i = 0; i < per && i < 8; i++) {
+      const int d = threadIdx.x * per + i;
+      if (d < nv) {
+        const int r = in.d2r[v0 + d];
+        rb[i] = in.rp[r];
+        local += (int)(in.rp[r + 1] - rb[i]);
+      }
+    }
+    for (int i = 8; i < per; i++) {
+      const int d = threadIdx.x * per + i;
+      if (d < nv) {
+        const int r = in.d2r[v0 + d];
+        local += (int)(in.rp[r + 1] - in.rp[r]);
+      }
+    }
+    int base;
+    BS(scan_tmp).ExclusiveSum(local, base);
+    for (int i = 0; i < per; i++) {
+      const int d = threadIdx.x * per + i;
+      if (d >= nv) break;
+      int64_t b;
+      int dd;
+      if (i < 8) {
+        b = rb[i];
+        dd = (int)(in.rp[in.d2r[v0 + d] + 1] - b);
+      } else {
+        const int r = in.d2r[v0 + d];
+        b = in.rp[r];
+        dd = (int)(in.rp[r + 1] - b);
+      }
+      off[d] = base;
+      for (int j = 0; j < dd; j++) adj[base + j] = in.r2d[in.col[b + j]] - (int)v0;
+      base += dd;
+    }
+    if (threadIdx.x == NT - 1) off[nv] = base;
+    R.off = off;
+    R.adj = adj;
+  } else {
+    R.rp = in.rp;
+    R.col = in.col;
+  }
+  __syncthreads();
+  // --- the marks protocol, one edge per thread: _micro_edge (census.py:
+  // 190-256) for the per-edge table, _count_edge (259-303: d(lo) <= d(hi),
+  // half the sweeps) for the global census.  Vertex labels: local dense ids
+  // (batch) or rank ids (one graph); the w < y tests only need some fixed
+  // total order to count each edge once.  The graph is small (n <= 8192), so
+  // per-edge counts fit 32 bits and the 13 sums of a CTA fit 64 bits.
+  const LaneMarks mk{marks + threadIdx.x, NT};
+  const long long n = nv, m = e1 - e0;
+  u64 acc[kNumSums];
+  for (int k = 0; k < kNumSums; k++) acc[k] = 0;
+  u64 cnt = 0;
+  const int64_t first = e0 + (BATCH ? 0 : (int64_t)blockIdx.x * NT) + threadIdx.x;
+  const int64_t step = BATCH ? NT : (int64_t)gridDim.x * NT;
+  for (int64_t e = first; e < e1; e += step) {
+    int u = BATCH ? in.eu[e] - (int)v0 : in.d2r[in.eu[e]];
+    int v = BATCH ? in.ev[e] - (int)v0 : in.d2r[in.ev[e]];
+    const bool flip = !table && R.deg(u) > R.deg(v);  // _count_edge orientation
+    if (flip) {
+      const int x = u;
+      u = v;
+      v = x;
+    }
+    const auto* au = R.row(u);
+    const auto* av = R.row(v);
+    const int du = R.deg(u), dv = R.deg(v);
+    for (int i = 0; i < du; i++) mk.set(au[i], 1);
+    mk.set(v, 0);
+    int t = 0, su = 0, sv = 0;
+    for (int i = 0; i < dv; i++) {
+      const int w = av[i];
+      if (mk.get(w) == 1) {
+        mk.set(w, 2);
+        t++;
+      } else if (w != u) {
+        mk.set(w, 3);
+        sv++;
+      }
+    }
+    for (int i = 0; i < du; i++) su += mk.get(au[i]) == 1;
+    int cl = 0, ts = 0, tdeg = 0, cy = 0, uu = 0, vv = 0, sdeg = 0;
+    for (int i = 0; i < dv; i++) {  // Tri sweep (census.py:215-225 / 286-291)
+      const int w = av[i];
+      if (mk.get(w) != 2) continue;
+      const auto* aw = R.row(w);
+      const int dw = R.deg(w);
+      tdeg += dw;
+      for (int k = 0; k < dw; k++) {
+        const int y = aw[k];
+        const unsigned mr = mk.get(y);
+        if (mr == 2) cl += w < y;
+        else if (mr) ts++;
+      }
+    }
+    for (int i = 0; i < du; i++) {  // Star_u sweep (census.py:227-236 / 292-299)
+      const int w = au[i];
+      if (mk.get(w) != 1) continue;
+      const auto* aw = R.row(w);
+      const int dw = R.deg(w);
+      sdeg += dw;
+      for (int k = 0; k < dw; k++) {
+        const int y = aw[k];
+        const unsigned mr = mk.get(y);
+        if (mr == 3) cy++;
+        else if (mr == 1 && w < y) uu++;
+      }
+    }
+    if (table) {
+      for (int i = 0; i < dv; i++) {  // Star_v sweep (census.py:238-244)
+        const int w = av[i];
+        if (mk.get(w) != 3) continue;
+        const auto* aw = R.row(w);
+        const int dw = R.deg(w);
+        sdeg += dw;
+        for (int k = 0; k < dw; k++) {
+          const int y = aw[k];
+          vv += mk.get(y) == 3 && w < y;
+        }
+      }
+    }
+    for (int i = 0; i < du; i++) mk.set(au[i], 0);  // census.py:252-255
+    for (int i = 0; i < dv; i++) mk.set(av[i], 0);
+    if (flip) {  // back to the canonical (u, v) sides
+      const int x = su;
+      su = sv;
+      sv = x;
+    }
+    // _census_batch (census.py:449-462) in 64 bits (small graph)
+    const u64 i3 = (u64)(n - 2 - t - su - sv);
+    acc[0] += t;
+    acc[1] += su + sv;
+    acc[2] += i3;
+    acc[3] += cl;
+    acc[4] += cy;
+    acc[5] += (u64)t * (t - 1) / 2;
+    acc[6] += (u64)su * sv;
+    acc[7] += (u64)t * (su + sv);
+    acc[8] += (u64)su * (su - 1) / 2 + (u64)sv * (sv - 1) / 2;
+    acc[9] += (u64)t * i3;
+    acc[10] += (u64)(su + sv) * i3;
+    acc[11] += i3 * (i3 - 1) / 2;
+    acc[12] += (u64)(m + 1 - (t + su + 1) - (t + sv + 1));
+    cnt++;
+    if (table) {
+      const long long ti = (long long)tdeg - 2 * t - 2 * cl - ts;                      // 246-247
+      const long long si = (long long)sdeg - su - sv - ts - 2 * (uu + vv) - 2 * cy;  // 248-250
+      const long long row[kNumMicro] = {t, su, sv, cl, cy, uu, vv, ts, ti, si};
+      store_row(table, e, row);
+    }
+  }
+  typedef cub::BlockReduce<u64, NT> BR;
+  __shared__ typename BR::TempStorage tmp2;
+  u64* out = sums + (size_t)gi * 2 * kNumSums;
+  for (int k = 0; k < kNumSums; k++) {
+    const u64 v = BR(tmp2).Sum(acc[k]);
+    if (threadIdx.x == 0 && v) atomic_add_u128(out + 2 * k, (u128)v);
+    __syncthreads();
+  }
+  const u64 c = BR(tmp2).Sum(cnt);
+  if (threadIdx.x == 0 && c) atomicAdd(seen + gi, c);
+}
+
 // ---- multi-GPU ownership (gd_count.cuh: Shard) ----------------------------
 // per-edge partials of passes B and C in rank-major blocks [W][4][M]: the
 // block of rank r holds the 4 fields of its owned edges [r*M, (r+1)*M)
@@ -1831,6 +2065,7 @@ void set_smem(K kernel, size_t bytes) {
 // every frame through one kernel variant so each variant can be checked
 // against the oracle on small graphs.  Results never depend on the path.
 struct ForcePaths {
+  bool any = false;
   bool tri_gmem = false, tri_small = false, tri_blocks = false, c4_smem = false,
        c4_coop = false, c4_hub32 = false, c4_flow = false, c4_cluster = false,
        c4_tile64 = false;
@@ -1841,6 +2076,7 @@ ForcePaths read_force() {
   const char* e = getenv("GD_FORCE_PATH");
   if (!e) return f;
   const std::string v(e);
+  f.any = !v.empty();
   f.tri_gmem = v.find("tri_gmem") != std::string::npos;
   f.tri_small = v.find("tri_small") != std::string::npos;
   f.tri_blocks = v.find("tri_blocks") != std::string::npos;
@@ -1887,6 +2123,66 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     ex.stats.push_back(val);
     ex.stats_names.push_back(name);
   };
+
+  // ---- small graphs: one direct kernel (k_small_census) --------------------
+  if (m > 0 && world == 1 && !force.any && env_int("GD_SMALL", 1) != 0) {
+    std::vector<int64_t> voff(G + 1, 0), eoff(G + 1, 0);
+    if (G == 1) {
+      voff[1] = n;
+      eoff[1] = m;
+    } else {
+      for (int64_t i = 0; i < G; i++) voff[i + 1] = voff[i] + g.h_gn[i];
+      eoff = g.h_eoff;
+    }
+    int64_t nmax = 0, stage = 0;
+    for (int64_t i = 0; i < G; i++) {
+      const int64_t nv = voff[i + 1] - voff[i], mg = eoff[i + 1] - eoff[i];
+      nmax = std::max(nmax, nv);
+      stage = std::max(stage, 4 * (nv + 1) + 8 * mg);
+    }
+    // one thread per edge with 2-bit marks over the graph's vertices: the
+    // graph must be small (counts then fit 32 bits) and fit shared memory
+    const int NT = G > 1 ? 256 : 128;
+    const int64_t words = (nmax + 15) / 16;
+    const int64_t smem = 4 * words * NT + (G > 1 ? stage : 0);
+    const int64_t limit = env_int("GD_SMALL_SMEM", 160 * 1024);
+    // (64-bit sums per CTA: m_g * C(n_g, 2) < 2^64 for n_g <= 8192)
+    if (nmax <= 8192 && smem <= limit) {
+      DBuf<int64_t> dvo, deo;
+      dvo.alloc(G + 1, s);
+      GD_CUDA(cudaMemcpyAsync(dvo.p, voff.data(), (G + 1) * 8, cudaMemcpyHostToDevice, s));
+      const int64_t* eo = g.eoff.p;
+      if (G == 1) {
+        deo.alloc(2, s);
+        GD_CUDA(cudaMemcpyAsync(deo.p, eoff.data(), 2 * 8, cudaMemcpyHostToDevice, s));
+        eo = deo.p;
+      }
+      SmallIn in{g.rp.p, g.col.p, g.eu.p, g.ev.p, g.d2r.p, g.r2d.p, dvo.p, eo};
+      GD_CUDA(cudaMemsetAsync(sums_dev, 0, (size_t)G * 2 * kNumSums * 8, s));
+      GD_CUDA(cudaMemsetAsync(seen_dev, 0, (size_t)G * 8, s));
+#define GD_SMALL_LAUNCH(NTV, BATCH)                                                           \
+  {                                                                                           \
+    auto kern = k_small_census<NTV, BATCH>;                                                   \
+    set_smem(kern, (size_t)smem);                                                             \
+    int occ = 1;                                                                              \
+    GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NTV, (size_t)smem));    \
+    const int64_t grid = G > 1 ? G : std::min<int64_t>((m + NTV - 1) / NTV,                   \
+                                                       (int64_t)std::max(occ, 1) * num_sms()); \
+    kern<<<(int)grid, NTV, (size_t)smem, s>>>(in, (int)G, (int)words, table_dev, sums_dev,    \
+                                              seen_dev);                                      \
+  }
+      if (G > 1) GD_SMALL_LAUNCH(256, true) else GD_SMALL_LAUNCH(128, false)
+#undef GD_SMALL_LAUNCH
+      GD_LAUNCH_CHECK("small_census");
+      timer.mark("small");
+      timer.collect(ex.ms, ex.names);
+      stat("small_graph_path", 1);
+      stat("launches", g_launches - launches0);
+      stat("shards", 1);
+      ex.direct = true;
+      return;
+    }
+  }
 
   // slot-indexed accumulators (workspace buffers, zeroed per call)
   struct WBuf { u64* p; };

@@ -16,6 +16,7 @@ struct CensusExtras {
   std::vector<std::string> names;
   std::vector<int64_t> stats;
   std::vector<std::string> stats_names;
+  bool direct = false;  // small-graph path: sums complete, no 4-clique / 4-cycle totals
   int64_t row0 = 0;   // first canonical edge of the rows written to the table
   int64_t rows = -1;  // rows written (-1: all m)
 };

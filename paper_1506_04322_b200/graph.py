@@ -11,7 +11,6 @@ when they are read.  Any object exposing ``n`` and ``edges`` (a reference
 from __future__ import annotations
 
 import ctypes
-import threading
 from dataclasses import dataclass
 from typing import Iterable, Sequence
 
@@ -59,6 +58,9 @@ class _Handle:
 
 
 def _as_pairs(pairs) -> np.ndarray:
+    if isinstance(pairs, np.ndarray) and pairs.dtype == np.int64 and pairs.ndim == 2 and \
+            pairs.shape[1] == 2 and pairs.flags.c_contiguous:
+        return pairs
     if isinstance(pairs, np.ndarray):
         arr = pairs
     else:
@@ -206,20 +208,6 @@ class Graph:
         return f"Graph(n={self.n}, m={self.m}, device)"
 
 
-_staging = threading.local()
-
-
-def _staging_pairs(k: int) -> np.ndarray:
-    """A (k, 2) int64 view of this thread's pinned staging buffer (grown
-    geometrically, never shrunk; pageable if pinning fails)."""
-    buf = getattr(_staging, "buf", None)
-    if buf is None or len(buf) < k:
-        buf = N.pinned_empty((max(k, 2 * (len(buf) if buf is not None else 0), 1024), 2),
-                             np.int64)
-        _staging.buf = buf
-    return buf[:k]
-
-
 class GraphBatch:
     """Many independent graphs packed as one device graph (disjoint union),
     counted in one launch sequence (config 4; replaces feature_matrix's
@@ -234,15 +222,14 @@ class GraphBatch:
         arrs = [_as_pairs(p) for p in pairs_list]
         offs = np.zeros(len(arrs) + 1, dtype=np.int64)
         np.cumsum([len(a) for a in arrs], out=offs[1:])
-        # packed into this thread's page-locked staging buffer (reused across
-        # batches: no fresh pages to fault in, and a DMA-able H2D source)
-        flat = _staging_pairs(int(offs[-1]))
-        if offs[-1]:
-            np.concatenate(arrs, out=flat)
+        # the library gathers the per-graph arrays into its page-locked
+        # staging with all host cores (no packing pass here)
+        ptrs = np.fromiter((a.__array_interface__["data"][0] for a in arrs), dtype=np.uint64,
+                           count=len(arrs))
         ns = np.ascontiguousarray(np.asarray(n_list, dtype=np.int64))
         out = ctypes.c_void_p()
-        N.check(N.lib().gd_graph_create_batch(N.vptr(flat), N.ptr(offs), N.ptr(ns), len(arrs), 0,
-                                              ctypes.byref(out)))
+        N.check(N.lib().gd_graph_create_batch_list(ctypes.c_void_p(ptrs.ctypes.data), N.ptr(offs),
+                                                   N.ptr(ns), len(arrs), 0, ctypes.byref(out)))
         self._h = _Handle(out.value)
         self.num_graphs = len(arrs)
         self.n_per_graph = np.zeros(self.num_graphs, dtype=np.int64)

@@ -64,7 +64,7 @@ def test_degenerate_graphs():
 FORCED = ["tri_gmem", "tri_small", "tri_blocks", "c4_coop", "c4_hub32", "c4_smem",
           "c4_flow", "tri_gmem,c4_coop", "tri_small,c4_hub32", "wide_slots", "c4_flow,wide_slots",
           "c4_tile64", "c4_coop,c4_tile64", "c4_coop,c4_tile64,wide_slots", "c4_coop,c4_cluster",
-          "c4_coop,c4_flow"]
+          "c4_coop,c4_flow", "pipeline"]
 
 
 def _dense_cases():
@@ -103,6 +103,8 @@ for name, n, edges in T._dense_cases():
 print("ok")
 ''' % (str(GOLDEN.parent.parent), str(GOLDEN.parent))
     env = dict(os.environ, GD_FORCE_PATH=force)
+    if force == "pipeline":  # the multi-pass pipeline where the small-graph kernel would run
+        env = dict(os.environ, GD_SMALL="0")
     if "wide_slots" in force:  # 64-bit per-slot sums even where 32 bits suffice
         env["GD_WIDE_SLOTS"] = "1"
     if force == "tri_small,c4_hub32":
@@ -306,3 +308,43 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_small_graph_kernel_and_pipeline_agree():
+    """The one-launch small-graph kernel (reference marks protocol) and the
+    multi-pass pipeline give identical tables on the golden graphs and the
+    dense cases; the small path is the one taken by default for them."""
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import paper_1506_04322_b200 as gd
+from helpers import small_graphs
+import test_gpu_parity as T
+out = []
+for name, n, edges, counts, micro in small_graphs():
+    if not len(edges):
+        continue
+    g = gd.Graph(n, edges)
+    tab, f = gd.micro_census_table(g)
+    out.append((np.asarray(tab).copy(), f.counts, gd.last_stats(g).get("small_graph_path", 0)))
+for name, n, edges in T._dense_cases():
+    g = gd.Graph(n, edges)
+    tab, f = gd.micro_census_table(g)
+    out.append((np.asarray(tab).copy(), f.counts, gd.last_stats(g).get("small_graph_path", 0)))
+np.save(sys.argv[1], np.array(out, dtype=object), allow_pickle=True)
+print("ok")
+''' % (str(GOLDEN.parent.parent), str(GOLDEN.parent))
+    import tempfile
+    res = {}
+    with tempfile.TemporaryDirectory() as d:
+        for small in ("1", "0"):
+            path = os.path.join(d, f"r{small}.npy")
+            r = subprocess.run([sys.executable, "-c", code, path], capture_output=True, text=True,
+                               timeout=600, env=dict(os.environ, GD_SMALL=small))
+            assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+            res[small] = np.load(path, allow_pickle=True)
+    assert len(res["1"]) == len(res["0"])
+    assert sum(int(x[2]) for x in res["1"]) >= len(res["1"]) - 8  # default: mostly the small path
+    assert sum(int(x[2]) for x in res["0"]) == 0
+    for a, b in zip(res["1"], res["0"]):
+        assert np.array_equal(a[0], b[0]) and a[1] == b[1]
