@@ -2,6 +2,8 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <cstdlib>
 #include <algorithm>
@@ -244,6 +246,12 @@ static void store_timings(gd_graph* h, CensusExtras& ex) {
 static void census(gd_graph* h, bool per_edge, int64_t* table, int flags, uint64_t* sums,
                    int64_t* seen, const Shard& shard = Shard()) {
   std::lock_guard<std::mutex> lock(h->mu);
+  static const bool prof = getenv("GD_HOST_PROFILE") != nullptr;
+  std::vector<std::pair<const char*, std::chrono::steady_clock::time_point>> tp;
+  auto mark = [&](const char* w) {
+    if (prof) tp.push_back({w, std::chrono::steady_clock::now()});
+  };
+  mark("start");
   DevGraph& g = h->g;
   cudaStream_t s = h->s;
   const int64_t G = g.G;
@@ -264,20 +272,31 @@ static void census(gd_graph* h, bool per_edge, int64_t* table, int flags, uint64
     }
   }
   CensusExtras ex;
+  mark("alloc");
   run_census(g, per_edge, tptr, dsums.p, dseen.p, ex, s, shard);
+  mark("run_census");
   if (ex.rows >= 0 && (ex.row0 != r0 || ex.rows != r1 - r0))
     throw Error(GD_ECUDA, "shard row range mismatch");
-  std::vector<uint64_t> hs(G * 2 * kNumSums);
-  std::vector<int64_t> hseen(G);
-  GD_CUDA(cudaMemcpyAsync(hs.data(), dsums.p, hs.size() * 8, cudaMemcpyDeviceToHost, s));
-  GD_CUDA(cudaMemcpyAsync(hseen.data(), dseen.p, G * 8, cudaMemcpyDeviceToHost, s));
+  // sums and counts through this thread's page-locked result block
+  const size_t ns = (size_t)G * 2 * kNumSums;
+  uint64_t* pin = (uint64_t*)host_results((ns + G) * 8);
+  GD_CUDA(cudaMemcpyAsync(pin, dsums.p, ns * 8, cudaMemcpyDeviceToHost, s));
+  GD_CUDA(cudaMemcpyAsync(pin + ns, dseen.p, G * 8, cudaMemcpyDeviceToHost, s));
   if (dtable.p && r1 > r0) copy_d2h(table, dtable.p, (size_t)(r1 - r0) * kNumMicro * 8, s);
   GD_CUDA(cudaStreamSynchronize(s));
+  mark("d2h");
   store_timings(h, ex);
   ensure_pool_headroom(s);
-  if (!ex.direct) close_cycles(hs.data(), ex, G, per_edge);
-  if (sums) std::memcpy(sums, hs.data(), hs.size() * 8);
-  if (seen) std::memcpy(seen, hseen.data(), G * 8);
+  mark("headroom");
+  if (!ex.direct) close_cycles(pin, ex, G, per_edge);
+  if (sums) std::memcpy(sums, pin, ns * 8);
+  if (seen) std::memcpy(seen, pin + ns, G * 8);
+  if (prof) {
+    for (size_t i = 1; i < tp.size(); i++)
+      fprintf(stderr, "%s %.1f us  ", tp[i].first,
+              std::chrono::duration<double, std::micro>(tp[i].second - tp[i - 1].second).count());
+    fprintf(stderr, "\n");
+  }
 }
 
 }  // namespace gd

@@ -170,6 +170,8 @@ void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
 // never shrunk; valid until the next call on the same thread), and the
 // parallel gather of per-graph pair arrays into it.
 void* host_staging(size_t bytes);
+// A second per-thread page-locked block for small per-call results (sums).
+void* host_results(size_t bytes);
 void gather_pairs(const int64_t* const* lists, const int64_t* offs, int64_t G, int64_t* flat);
 
 // ---------------------------------------------------------------------------

@@ -113,6 +113,32 @@ void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   for (size_t c = nchunks > (size_t)kSlots ? nchunks - kSlots : 0; c < nchunks; c++) drain(c);
 }
 
+namespace {
+struct Block {
+  void* p = nullptr;
+  size_t n = 0;
+  ~Block() {
+    if (p) cudaFreeHost(p);
+  }
+  void* get(size_t bytes) {
+    if (n < bytes) {
+      const size_t want = std::max(bytes, n * 2);
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      n = 0;
+      GD_CUDA(cudaHostAlloc(&p, want, cudaHostAllocDefault));
+      n = want;
+    }
+    return p;
+  }
+};
+}  // namespace
+
+void* host_results(size_t bytes) {
+  static thread_local Block b;
+  return b.get(bytes);
+}
+
 void* host_staging(size_t bytes) {
   struct Block {
     void* p = nullptr;

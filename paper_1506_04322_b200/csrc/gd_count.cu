@@ -1582,8 +1582,9 @@ struct SmallIn {
   const int32_t* ev;
   const int32_t* d2r;
   const int32_t* r2d;
-  const int64_t* voff;  // [G+1] dense vertex offset of each graph
-  const int64_t* eoff;  // [G+1] canonical edge offset of each graph
+  const int64_t* voff;  // [G+1] dense vertex offset of each graph (batch)
+  const int64_t* eoff;  // [G+1] canonical edge offset of each graph (batch)
+  int64_t n1, m1;       // one graph: vertex and edge count
 };
 
 // 2-bit marks, private to one thread, laid out word-major / lane-minor so the
@@ -1617,17 +1618,18 @@ struct SharedRows {
   __device__ __forceinline__ const int* row(int x) const { return adj + off[x]; }
 };
 
-template <int NT, bool BATCH>
+template <int NT, bool BATCH, bool STAGE>
 __global__ void __launch_bounds__(NT)
 k_small_census(SmallIn in, int G, int words, long long* __restrict__ table,
                u64* __restrict__ sums, u64* __restrict__ seen) {
   extern __shared__ __align__(16) int sm_i[];
   const int gi = BATCH ? blockIdx.x : 0;
-  const int64_t v0 = in.voff[gi], e0 = in.eoff[gi], e1 = in.eoff[gi + 1];
-  const int nv = (int)(in.voff[gi + 1] - v0);
+  const int64_t v0 = BATCH ? in.voff[gi] : 0, e0 = BATCH ? in.eoff[gi] : 0;
+  const int64_t e1 = BATCH ? in.eoff[gi + 1] : in.m1;
+  const int nv = (int)(BATCH ? in.voff[gi + 1] - v0 : in.n1);
   unsigned* marks = (unsigned*)sm_i;  // [words][NT]
   for (int i = threadIdx.x; i < words * NT; i += NT) marks[i] = 0u;
-  typename std::conditional<BATCH, SharedRows, GlobalRows>::type R;
+  typename std::conditional<BATCH || STAGE, SharedRows, GlobalRows>::type R;
   if constexpr (BATCH) {
     // stage the graph in local dense ids: degrees, offsets (block scan),
     // rows (thread per vertex, its row converted rank -> local dense)
@@ -1673,6 +1675,16 @@ k_small_census(SmallIn in, int G, int words, long long* __restrict__ table,
       base += dd;
     }
     if (threadIdx.x == NT - 1) off[nv] = base;
+    R.off = off;
+    R.adj = adj;
+  } else if constexpr (STAGE) {
+    // one graph that fits: its rank CSR copied as is (coalesced) -- every
+    // later access is a shared-memory load
+    int* off = (int*)(marks + (size_t)words * NT);  // [n + 1]
+    int* adj = off + nv + 1;                        // [2 m]
+    for (int i = threadIdx.x; i <= nv; i += NT) off[i] = (int)in.rp[i];
+    const int two_m = (int)(2 * (e1 - e0));
+    for (int i = threadIdx.x; i < two_m; i += NT) adj[i] = in.col[i];
     R.off = off;
     R.adj = adj;
   } else {
@@ -2144,25 +2156,25 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     // graph must be small (counts then fit 32 bits) and fit shared memory
     const int NT = G > 1 ? 256 : 128;
     const int64_t words = (nmax + 15) / 16;
-    const int64_t smem = 4 * words * NT + (G > 1 ? stage : 0);
+    // one graph: its CSR is staged too when it fits beside the marks
+    const bool stage_one = G == 1 && 4 * words * NT + stage <= env_int("GD_SMALL_SMEM", 160 * 1024);
+    const int64_t smem = 4 * words * NT + (G > 1 || stage_one ? stage : 0);
     const int64_t limit = env_int("GD_SMALL_SMEM", 160 * 1024);
     // (64-bit sums per CTA: m_g * C(n_g, 2) < 2^64 for n_g <= 8192)
     if (nmax <= 8192 && smem <= limit) {
-      DBuf<int64_t> dvo, deo;
-      dvo.alloc(G + 1, s);
-      GD_CUDA(cudaMemcpyAsync(dvo.p, voff.data(), (G + 1) * 8, cudaMemcpyHostToDevice, s));
-      const int64_t* eo = g.eoff.p;
-      if (G == 1) {
-        deo.alloc(2, s);
-        GD_CUDA(cudaMemcpyAsync(deo.p, eoff.data(), 2 * 8, cudaMemcpyHostToDevice, s));
-        eo = deo.p;
+      DBuf<int64_t> dvo;
+      SmallIn in{g.rp.p, g.col.p, g.eu.p, g.ev.p, g.d2r.p, g.r2d.p, nullptr, nullptr, n, m};
+      if (G > 1) {
+        dvo.alloc(G + 1, s);
+        GD_CUDA(cudaMemcpyAsync(dvo.p, voff.data(), (G + 1) * 8, cudaMemcpyHostToDevice, s));
+        in.voff = dvo.p;
+        in.eoff = g.eoff.p;
       }
-      SmallIn in{g.rp.p, g.col.p, g.eu.p, g.ev.p, g.d2r.p, g.r2d.p, dvo.p, eo};
       GD_CUDA(cudaMemsetAsync(sums_dev, 0, (size_t)G * 2 * kNumSums * 8, s));
       GD_CUDA(cudaMemsetAsync(seen_dev, 0, (size_t)G * 8, s));
-#define GD_SMALL_LAUNCH(NTV, BATCH)                                                           \
+#define GD_SMALL_LAUNCH(NTV, BATCH, STAGE)                                                    \
   {                                                                                           \
-    auto kern = k_small_census<NTV, BATCH>;                                                   \
+    auto kern = k_small_census<NTV, BATCH, STAGE>;                                            \
     set_smem(kern, (size_t)smem);                                                             \
     int occ = 1;                                                                              \
     GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NTV, (size_t)smem));    \
@@ -2171,7 +2183,9 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     kern<<<(int)grid, NTV, (size_t)smem, s>>>(in, (int)G, (int)words, table_dev, sums_dev,    \
                                               seen_dev);                                      \
   }
-      if (G > 1) GD_SMALL_LAUNCH(256, true) else GD_SMALL_LAUNCH(128, false)
+      if (G > 1) GD_SMALL_LAUNCH(256, true, false)
+      else if (stage_one) GD_SMALL_LAUNCH(128, false, true)
+      else GD_SMALL_LAUNCH(128, false, false)
 #undef GD_SMALL_LAUNCH
       GD_LAUNCH_CHECK("small_census");
       timer.mark("small");
