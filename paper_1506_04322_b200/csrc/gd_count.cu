@@ -220,6 +220,35 @@ __device__ __forceinline__ void for_frame_items(const View& g, const int* P, con
   constexpr int K = GD_TRI_K, U = GD_TRI_U;
   constexpr int NW = NT / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifndef GD_TRI_NO_PREFETCH
+  // rolling prefetch: the col[] load of the lane's next item is issued
+  // before the current item is processed (one load in flight while the
+  // hash probe of the previous one runs; 3 extra registers)
+  for (int c0 = warp * 32 * K; c0 < total; c0 += NW * 32 * K) {
+    const int c1 = min(c0 + 32 * K, total);
+    int i = c0 + lane;
+    if (i >= c1) continue;
+    int j = find_segment(P, D, i);
+    int pj1 = P[j + 1];
+    int64_t q = QB[j] + i;
+    int y = __ldg(g.col + q);
+    for (; i < c1; i += 32) {
+      const int ni = i + 32;
+      int jn = j;
+      int64_t qn = 0;
+      int yn = 0;
+      if (ni < c1) {
+        while (pj1 <= ni) pj1 = P[++jn + 1];
+        qn = QB[jn] + ni;
+        yn = __ldg(g.col + qn);
+      }
+      f(j, i, q, y);
+      j = jn;
+      q = qn;
+      y = yn;
+    }
+  }
+#else
   for (int c0 = warp * 32 * K; c0 < total; c0 += NW * 32 * K) {
     const int c1 = min(c0 + 32 * K, total);
     int i = c0 + lane;
@@ -247,6 +276,7 @@ __device__ __forceinline__ void for_frame_items(const View& g, const int* P, con
         if (i + 32 * u < c1) f(jj[u], i + 32 * u, qq[u], yy[u]);
     }
   }
+#endif
 }
 
 // Set bit b of a 64-bit-word bitmap row with a native 32-bit atomicOr (a
@@ -1357,6 +1387,26 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
                                   }
                                 });
           } else {
+#ifndef GD_TILE_RUNSCAN
+            // per-lane running sum of its current segment, flushed to the
+            // segment's shared slot sum when the lane moves on (lanes of a
+            // long segment flush once per segment; no cross-lane scan)
+            int cur_k = -1;
+            SumT cur = 0;
+            tile_range_items<U>(g, seg_pre, seg_off, ncomp, r0, r1,
+                                [&](int k, int64_t q, int x, unsigned) {
+              if (k < 0) return;
+              const SumT c = (SumT)((unsigned)tile16[x - X] - 1u);
+              if (c) red_add(&c4s[q], (CT)c);  // edge w-x
+              if (k != cur_k) {
+                if (cur) atomicAdd(&seg_sum[cur_k], cur);
+                cur_k = k;
+                cur = 0;
+              }
+              cur += c;
+            });
+            if (cur) atomicAdd(&seg_sum[cur_k], cur);
+#else
             tile_range_items<U>(g, seg_pre, seg_off, ncomp, r0, r1,
                                 [&](int k, int64_t q, int x, unsigned M) {
               SumT c = 0;
@@ -1381,6 +1431,7 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
               const bool end = lane == 31 || ((M >> (lane + 1)) & 1u) || kn != k;
               if (k >= 0 && end && run) atomicAdd(&seg_sum[k], run);
             });
+#endif
           }
         }
         __syncthreads();

@@ -6,7 +6,7 @@ import os, subprocess, sys
 cfg, mode, libs = sys.argv[1], sys.argv[2], sys.argv[3:]
 code = r'''
 import sys, json, hashlib
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, %r)
 import numpy as np, torch
 import paper_1506_04322_b200 as gd
 from paper_1506_04322_b200 import _native as N, workloads as W
@@ -31,7 +31,7 @@ h = hashlib.sha256(repr(sorted(f.counts.items())).encode() if f else b"failed")
 if %r == "per_edge" and f:
     h.update(t.cpu().numpy().tobytes())
 print(json.dumps({k: round(v, 2) for k, v in tm.items()}), "total_ms %%.2f" %% (sum(tot) / len(tot)), "digest", h.hexdigest()[:16])
-''' % (cfg, mode, mode)
+''' % (str(__import__('pathlib').Path(__file__).resolve().parent.parent), cfg, mode, mode)
 for lib in libs:
     env = dict(os.environ)
     if "=" in lib:  # NAME=VALUE: the default library under an env setting
