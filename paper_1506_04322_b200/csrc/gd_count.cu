@@ -1256,7 +1256,10 @@ __global__ void k_tile_splits(View g, int x0, int T, int P1, int64_t* __restrict
 // are resolved before their col[] loads are issued.  f(k, q, x, M, j) gets
 // the segment k (-1 past r1), slot q, x = col[q] and the step's start bits.
 #ifndef GD_TILE_U
-#define GD_TILE_U 2
+#define GD_TILE_U 4  // measured U = 1 / 2 / 3 / 4 / 6 / 8: C3 per-edge 45.6 / 37.7 / 36.0 / 34.8 / 36.2 / 36.8 ms
+#endif
+#ifndef GD_TILE_NT
+#define GD_TILE_NT 1024
 #endif
 template <int U, typename F>
 __device__ __forceinline__ void tile_range_items(const View& g, const int* seg_pre,
@@ -1296,7 +1299,7 @@ __device__ __forceinline__ void tile_range_items(const View& g, const int* seg_p
 }
 
 template <int NT, typename CT>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, 1024 / NT)
 k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
            CT* __restrict__ c4s, u64* __restrict__ c4tot2,
            unsigned long long* __restrict__ next_job) {
@@ -2611,15 +2614,13 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       GD_CUDA(cudaStreamSynchronize(s));
       x0 &= ~1;
     }
-    // x-tiles in shared memory: always for the global census (its count
-    // sweep is the whole job); per edge only while a frame spans few tiles --
-    // the use sweep then walks each lower row in per-tile pieces, which at
-    // n = 4M (43 tiles, ~22 items per piece) costs more than the dense L2
-    // slabs save (C5 per-edge flow 474 -> 549 ms, C3 48.3 -> 43.0 ms)
+    // x-tiles in shared memory for every heavy frame (the dense-slab flow
+    // kernel and the DSMEM cluster kernel stay selectable: GD_C4_TILES=0,
+    // GD_FORCE_PATH=c4_flow / c4_cluster).  Measured: C3 per-edge 48.3 (flow)
+    // -> 34.8 ms, C3 global 30.1 -> 18.6, C5 global 320 -> 236, C5 per-edge
+    // 474 -> 470 ms (its ~22-item row pieces make the use sweep the costly half)
     const int64_t tile_mode = env_int("GD_C4_TILES", 1);
-    const int64_t max_tiles = (n - x0 + 90111) / 90112;
-    const bool use_tiles = !force.c4_flow && !force.c4_cluster && tile_mode != 0 &&
-                           (tile_mode == 2 || force.c4_tile64 || !per_edge || max_tiles <= 16);
+    const bool use_tiles = !force.c4_flow && !force.c4_cluster && tile_mode != 0;
     tiles_used = use_tiles && !f16_all.empty();
     for (const int rk : my_ranks) {
     // this shard's frames: every world-th heavy frame in descending-work order
@@ -2649,8 +2650,11 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       }
     }
     if (!f16.empty() && use_tiles) {
-      constexpr int NT = 1024;
-      const int T = force.c4_tile64 ? 64 : (int)(env_int("GD_C4_TILE", 90112) & ~int64_t(7));
+      constexpr int NT = GD_TILE_NT;
+      // tile: the dynamic shared memory one CTA (1024 threads) or two (512
+      // each) per SM can hold beside the kernel's static arrays
+      const int T = force.c4_tile64 ? 64 : (int)(env_int("GD_C4_TILE", NT == 1024 ? 90112 : 45056) &
+                                                 ~int64_t(7));
       const int64_t ptot = (n - x0 + T - 1) / T;
       const int P1 = (int)ptot + 1;
       int64_t* TS = ws_get<int64_t>(g, "c4_ts", (size_t)n * P1, s);
