@@ -26,6 +26,7 @@
  * tests/test_crosscheck.py on the dense / C1 / C2 cases and on the C3 samples.
  */
 #include <omp.h>
+#include <stdio.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -132,19 +133,26 @@ static void triangle_pass(const XG* g, const int64_t* edges, int64_t* t, int64_t
     int32_t* mk1 = malloc(4 * (size_t)n);  /* edge id + 1 of (a, x), x in N+(a) */
     int32_t* mk2 = malloc(4 * (size_t)n);  /* edge id + 1 of (x, y), y in N+(a) & N+(x) */
     int32_t* L = malloc(4 * (size_t)n);
+    /* membership bitmaps in front of mk1 / mk2: n bits stay cache-resident
+       where the n-int arrays do not (most probes are misses) */
+    uint64_t* bm1 = calloc((size_t)(n >> 6) + 1, 8);
+    uint64_t* bm2 = calloc((size_t)(n >> 6) + 1, 8);
     memset(mk1, 0, 4 * (size_t)n);
     memset(mk2, 0, 4 * (size_t)n);
 #pragma omp for schedule(dynamic, 64)
     for (int64_t a = 0; a < n; a++) {
       const int64_t b = g->op[a], e_ = g->op[a + 1];
       if (e_ - b < 2) continue;
-      for (int64_t i = b; i < e_; i++) mk1[g->oadj[i]] = g->oeid[i] + 1;
+      for (int64_t i = b; i < e_; i++) {
+        mk1[g->oadj[i]] = g->oeid[i] + 1;
+        bm1[g->oadj[i] >> 6] |= 1ull << (g->oadj[i] & 63);
+      }
       for (int64_t i = b; i < e_; i++) {
         const int32_t x = g->oadj[i], eax = g->oeid[i];
         int64_t nl = 0;
         for (int64_t j = g->op[x]; j < g->op[x + 1]; j++) {
           const int32_t y = g->oadj[j];
-          if (!mk1[y]) continue;
+          if (!((bm1[y >> 6] >> (y & 63)) & 1)) continue;
           const int32_t exy = g->oeid[j], eay = mk1[y] - 1;
           /* triangle {a, x, y} */
           if (!second) {
@@ -155,6 +163,7 @@ static void triangle_pass(const XG* g, const int64_t* edges, int64_t* t, int64_t
             ADD(&T[x], 1);
             ADD(&T[y], 1);
             mk2[y] = exy + 1;
+            bm2[y >> 6] |= 1ull << (y & 63);
             L[nl++] = y;
           } else {
             /* edge (p, q) with third vertex r: t(p, r) to p's side,
@@ -181,7 +190,7 @@ static void triangle_pass(const XG* g, const int64_t* edges, int64_t* t, int64_t
           const int32_t eay = mk1[y] - 1, exy = mk2[y] - 1;
           for (int64_t j = g->op[y]; j < g->op[y + 1]; j++) {
             const int32_t z = g->oadj[j];
-            if (!mk2[z]) continue;
+            if (!((bm2[z >> 6] >> (z & 63)) & 1)) continue;
             ADD(&cl[eax], 1);
             ADD(&cl[eay], 1);
             ADD(&cl[mk1[z] - 1], 1);
@@ -190,56 +199,130 @@ static void triangle_pass(const XG* g, const int64_t* edges, int64_t* t, int64_t
             ADD(&cl[g->oeid[j]], 1);
           }
         }
-        for (int64_t li = 0; li < nl; li++) mk2[L[li]] = 0;
+        for (int64_t li = 0; li < nl; li++) {
+          mk2[L[li]] = 0;
+          bm2[L[li] >> 6] = 0;
+        }
       }
-      for (int64_t i = b; i < e_; i++) mk1[g->oadj[i]] = 0;
+      for (int64_t i = b; i < e_; i++) {
+        mk1[g->oadj[i]] = 0;
+        bm1[g->oadj[i] >> 6] = 0;
+      }
     }
     free(mk1);
     free(mk2);
+    free(bm1);
+    free(bm2);
     free(L);
   }
 }
 
-/* pass 3: C4(e) for every edge, from the higher endpoint's common-neighbour array */
+/* pass 3: C4(e) for every edge, from the higher endpoint's common-neighbour
+ * counts c(c, x).  Centres with a small 2-hop volume S(c) use one dense
+ * n-sized array; for the rest the x range is cut into tiles of 2^18 counters
+ * (1 MB, cache-resident) walked with per-row cursors -- the same counts, but
+ * a 4M-vertex graph's 1.4e12 increments no longer each miss the cache. */
 static void cycle_pass(const XG* g, int64_t* c4, int threads) {
   const int64_t n = g->n;
+  /* tile size and the S(c) above which a centre is tiled (tests shrink both) */
+  const char* ev = getenv("XC_TILE");
+  const int64_t XT_TILE = ev ? atoll(ev) : (1 << 18);
+  ev = getenv("XC_TILE_S");
+  const int64_t XT_S = ev ? atoll(ev) : 4 * XT_TILE;
 #pragma omp parallel num_threads(threads)
   {
     uint32_t* cnt = calloc((size_t)n, 4);
+    uint32_t* tile = calloc((size_t)XT_TILE, 4);
+    int64_t* curw = NULL;
+    int64_t* curl = NULL;
+    int64_t* acc = NULL;
+    int32_t* lows = NULL;
+    int64_t cap = 0;
 #pragma omp for schedule(dynamic, 16)
     for (int64_t c = 0; c < n; c++) {
-      /* lower neighbours lo of c: edges (lo, c) with c the higher endpoint */
-      int has = 0;
-      for (int64_t i = g->ip[c]; i < g->ip[c + 1] && !has; i++)
-        has = higher(g, g->adj[i], (int32_t)c);
-      if (!has) continue;
-      for (int64_t i = g->ip[c]; i < g->ip[c + 1]; i++) {
-        const int32_t w = g->adj[i];
-        for (int64_t j = g->ip[w]; j < g->ip[w + 1]; j++) cnt[g->adj[j]]++;
+      const int64_t b = g->ip[c], e_ = g->ip[c + 1], dc = e_ - b;
+      int64_t nlow = 0, S = 0;
+      for (int64_t i = b; i < e_; i++) {
+        nlow += higher(g, g->adj[i], (int32_t)c);
+        S += g->deg[g->adj[i]];
       }
-      for (int64_t i = g->ip[c]; i < g->ip[c + 1]; i++) {
-        const int32_t lo = g->adj[i];
-        if (!higher(g, lo, (int32_t)c)) continue;
+      if (!nlow) continue;
+      if (S <= XT_S) {
+        for (int64_t i = b; i < e_; i++) {
+          const int32_t w = g->adj[i];
+          for (int64_t j = g->ip[w]; j < g->ip[w + 1]; j++) cnt[g->adj[j]]++;
+        }
+      }
+      if (dc > cap) {
+        cap = dc;
+        curw = realloc(curw, 8 * (size_t)cap);
+        curl = realloc(curl, 8 * (size_t)cap);
+        acc = realloc(acc, 8 * (size_t)cap);
+        lows = realloc(lows, 4 * (size_t)cap);
+      }
+      nlow = 0;
+      for (int64_t i = b; i < e_; i++)
+        if (higher(g, g->adj[i], (int32_t)c)) lows[nlow++] = g->adj[i];
+      if (S <= XT_S) {
+        for (int64_t k = 0; k < nlow; k++) {
+          const int32_t lo = lows[k];
+          int64_t s = 0;
+          for (int64_t j = g->ip[lo]; j < g->ip[lo + 1]; j++) {
+            const int32_t x = g->adj[j];
+            if (x != c) s += (int64_t)cnt[x] - 1;
+          }
+          acc[k] = s;
+        }
+        for (int64_t i = b; i < e_; i++) {
+          const int32_t w = g->adj[i];
+          for (int64_t j = g->ip[w]; j < g->ip[w + 1]; j++) cnt[g->adj[j]] = 0;
+        }
+      } else {
+        for (int64_t i = 0; i < dc; i++) curw[i] = g->ip[g->adj[b + i]];
+        for (int64_t k = 0; k < nlow; k++) {
+          curl[k] = g->ip[lows[k]];
+          acc[k] = 0;
+        }
+        for (int64_t x0 = 0; x0 < n; x0 += XT_TILE) {
+          const int64_t x1 = x0 + XT_TILE;
+          for (int64_t i = 0; i < dc; i++) {
+            const int32_t w = g->adj[b + i];
+            int64_t p = curw[i];
+            const int64_t pe = g->ip[w + 1];
+            for (; p < pe && g->adj[p] < x1; p++) tile[g->adj[p] - x0]++;
+            curw[i] = p;
+          }
+          for (int64_t k = 0; k < nlow; k++) {
+            const int32_t lo = lows[k];
+            int64_t p = curl[k], s = 0;
+            const int64_t pe = g->ip[lo + 1];
+            for (; p < pe && g->adj[p] < x1; p++) {
+              const int32_t x = g->adj[p];
+              if (x != c) s += (int64_t)tile[x - x0] - 1;
+            }
+            curl[k] = p;
+            acc[k] += s;
+          }
+          memset(tile, 0, 4 * (size_t)XT_TILE);
+        }
+      }
+      for (int64_t k = 0; k < nlow; k++) {
         /* edge id of (lo, c): lo's oriented row holds c */
+        const int32_t lo = lows[k];
         int64_t a = g->op[lo], z = g->op[lo + 1];
         while (a < z) {
           int64_t mid = (a + z) >> 1;
           if (g->oadj[mid] < c) a = mid + 1; else z = mid;
         }
-        const int32_t e = g->oeid[a];
-        int64_t s = 0;
-        for (int64_t j = g->ip[lo]; j < g->ip[lo + 1]; j++) {
-          const int32_t x = g->adj[j];
-          if (x != c) s += (int64_t)cnt[x] - 1;
-        }
-        c4[e] = s;
-      }
-      for (int64_t i = g->ip[c]; i < g->ip[c + 1]; i++) {
-        const int32_t w = g->adj[i];
-        for (int64_t j = g->ip[w]; j < g->ip[w + 1]; j++) cnt[g->adj[j]] = 0;
+        c4[g->oeid[a]] = acc[k];
       }
     }
     free(cnt);
+    free(tile);
+    free(curw);
+    free(curl);
+    free(acc);
+    free(lows);
   }
 }
 
@@ -267,9 +350,14 @@ int crosscheck_table(const int64_t* edges, int64_t m, int64_t n, int threads, in
   int64_t* S = calloc((size_t)n + 1, 8);
   u128* acc = calloc((size_t)T_ * 13, sizeof(u128));
   if (!t || !cl || !su || !sv || !td || !c4 || !T || !S || !acc) return -1;
+  const int verbose = getenv("XC_VERBOSE") != NULL;
+  double t0 = omp_get_wtime();
   triangle_pass(&g, edges, t, cl, T, NULL, NULL, NULL, T_);
+  if (verbose) fprintf(stderr, "crosscheck: triangles + 4-cliques %.1f s\n", omp_get_wtime() - t0);
   triangle_pass(&g, edges, t, cl, T, su, sv, td, T_);
+  if (verbose) fprintf(stderr, "crosscheck: triangle-set sums %.1f s\n", omp_get_wtime() - t0);
   cycle_pass(&g, c4, T_);
+  if (verbose) fprintf(stderr, "crosscheck: 4-cycles %.1f s\n", omp_get_wtime() - t0);
 #pragma omp parallel for num_threads(T_) schedule(static, 4096)
   for (int64_t v = 0; v < n; v++) {
     int64_t s = 0;

@@ -72,3 +72,26 @@ def test_full_size_fixtures_are_pinned(name):
     if name in ("c3_rmat20", "c5_chung_lu_4m"):
         assert d["pinned_by"].get("oracle_micro_sample_rows") is True
         assert d["pinned_by"].get("oracle_count_sample_chunks") is True
+
+
+def test_crosscheck_tiled_cycle_pass():
+    """The tiled common-neighbour path (large centres at full size) gives the
+    same tables: every centre tiled, tiles of 64 and 1000 vertices."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, %r)
+from oracle import oracle as O
+import test_crosscheck as T
+for name, n, edges in T._cases():
+    rows, sums = O.crosscheck_table(edges, n, threads=2)
+    assert np.array_equal(rows, O.micro_rows(edges, n, threads=2)), name
+print("ok")
+''' % str(GOLDEN.parent.parent)
+    for tile in ("64", "1000"):
+        env = dict(__import__("os").environ, XC_TILE=tile, XC_TILE_S="0",
+                   PYTHONPATH=str(GOLDEN.parent))
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
