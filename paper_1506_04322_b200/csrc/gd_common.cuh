@@ -124,6 +124,7 @@ struct DevGraph {
   std::vector<int64_t> h_eoff, h_gn;
   uint64_t hit_cap = 0;      // entries of the persisted hit-list buffer
   bool hit_cap_known = false;
+  uint64_t hit_cap_used = 0; // capacity the last census of this graph got
 };
 
 // Census workspace: large scratch buffers (slot accumulators, item prefixes,
