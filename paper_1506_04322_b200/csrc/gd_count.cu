@@ -1261,9 +1261,9 @@ __global__ void k_tile_splits(View g, int x0, int T, int P1, int64_t* __restrict
 #ifndef GD_TILE_NT
 #define GD_TILE_NT 1024
 #endif
-template <int U, typename F>
+template <int U, typename QT, typename F>
 __device__ __forceinline__ void tile_range_items(const View& g, const int* seg_pre,
-                                                 const long long* seg_off, int cnt,
+                                                 const QT* seg_off, int cnt,
                                                  int r0, int r1, F&& f) {
   const int lane = threadIdx.x & 31;
   const unsigned le = 0xffffffffu >> (31 - lane);  // bits 0..lane
@@ -1274,21 +1274,44 @@ __device__ __forceinline__ void tile_range_items(const View& g, const int* seg_p
     if (seg_pre[mid] <= r0) lo = mid; else hi = mid;
   }
   int kc = lo;
+#ifndef GD_TILE_NOFAST
+  // start of the segment after kc (uniform): steps that end before it lie in
+  // segment kc and need no resolution
+  int nb = kc + 1 < cnt ? seg_pre[kc + 1] : INT_MAX;
+  QT off_kc = seg_off[kc];
+#endif
   for (int base = r0; base < r1; base += 32 * U) {
     int kk[U];
-    int64_t qq[U];
+    QT qq[U];
     unsigned mm[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
       const int wb = base + 32 * u;
+#ifndef GD_TILE_NOFAST
+      if (wb + 32 <= nb) {  // the whole step inside segment kc
+        kk[u] = wb + lane < r1 ? kc : -1;
+        qq[u] = off_kc + wb + lane;
+        mm[u] = 0u;
+        continue;
+      }
+#endif
       const int k = kc + 1 + lane;
-      const int r = (k < cnt ? seg_pre[k] : INT_MAX) - wb;
+      const int sp = k < cnt ? seg_pre[k] : INT_MAX;
+      const int r = sp - wb;
       const unsigned M = __reduce_or_sync(0xffffffffu, r < 32 ? 1u << r : 0u);
       const int ks = kc + __popc(M & le);
-      kc += __popc(M);
+      const int adv = __popc(M);
+      kc += adv;
       kk[u] = wb + lane < r1 ? ks : -1;
       qq[u] = seg_off[ks] + wb + lane;
       mm[u] = M;
+#ifndef GD_TILE_NOFAST
+      // lane adv loaded seg_pre[kc_new + 1] (re-read when all 32 lanes' segments
+      // started in this step); lane 31's slot gives seg_off[kc_new]
+      nb =__shfl_sync(0xffffffffu, sp, adv & 31);
+      if (adv == 32) nb = kc + 1 < cnt ? seg_pre[kc + 1] : INT_MAX;
+      off_kc = __shfl_sync(0xffffffffu, qq[u], 31) - (wb + 31);
+#endif
     }
     int xx[U];
 #pragma unroll
@@ -1298,7 +1321,9 @@ __device__ __forceinline__ void tile_range_items(const View& g, const int* seg_p
   }
 }
 
-template <int NT, typename CT>
+// QT: slot index type (int when every slot index fits 31 bits: one IMAD.WIDE
+// per address instead of 64-bit adds)
+template <int NT, typename CT, typename QT>
 __global__ void __launch_bounds__(NT, 1024 / NT)
 k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
            CT* __restrict__ c4s, u64* __restrict__ c4tot2,
@@ -1311,7 +1336,7 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
   extern __shared__ __align__(16) unsigned tile[];  // T u16 counters
   __shared__ long long s_job, s_next;
   __shared__ int s_range;
-  __shared__ long long seg_off[C];
+  __shared__ QT seg_off[C];
   __shared__ int seg_pre[C + 1];
   __shared__ SumT seg_sum[C];
   __shared__ int seg_slot[C];
@@ -1373,7 +1398,7 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
         const int pre = (int)(pk & 0xffffffffll), ci = (int)(pk >> 32);
         const int total = (int)(tot & 0xffffffffll), ncomp = (int)(tot >> 32);
         if (len > 0) {
-          seg_off[ci] = a - pre;
+          seg_off[ci] = (QT)(a - pre);
           seg_pre[ci] = pre;
           seg_slot[ci] = (int)(c0 + threadIdx.x);
         }
@@ -1393,7 +1418,7 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
           const int r1 = min(total, r0 + R);
           if (sweep == 0) {
             tile_range_items<U>(g, seg_pre, seg_off, ncomp, r0, r1,
-                                [&](int k, int64_t, int x, unsigned) {
+                                [&](int k, QT, int x, unsigned) {
                                   if (k >= 0) {
                                     const int xr = x - X;
                                     atomicAdd(&tile[xr >> 1], 1u << ((xr & 1) << 4));
@@ -1407,7 +1432,7 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
             int cur_k = -1;
             SumT cur = 0;
             tile_range_items<U>(g, seg_pre, seg_off, ncomp, r0, r1,
-                                [&](int k, int64_t q, int x, unsigned) {
+                                [&](int k, QT q, int x, unsigned) {
               if (k < 0) return;
               const SumT c = (SumT)((unsigned)tile16[x - X] - 1u);
               if (c) red_add(&c4s[q], (CT)c);  // edge w-x
@@ -1421,7 +1446,7 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
             if (cur) atomicAdd(&seg_sum[cur_k], cur);
 #else
             tile_range_items<U>(g, seg_pre, seg_off, ncomp, r0, r1,
-                                [&](int k, int64_t q, int x, unsigned M) {
+                                [&](int k, QT q, int x, unsigned M) {
               SumT c = 0;
               if (k >= 0) {
                 c = (SumT)((unsigned)tile16[x - X] - 1u);
@@ -2695,8 +2720,10 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       GD_CUDA(cudaMemcpyAsync(djf.p, jframe.data(), jframe.size() * 4, cudaMemcpyHostToDevice, s));
       TilePlan TP{dfr.p, djp.p, djf.p, (int)f16.size(), jpre.back(), x0, T, P1, TS};
       const size_t sm = (size_t)T * 2;
-      auto tk = k_c4_tiles<NT, u64>;
-      auto tk32 = k_c4_tiles<NT, unsigned>;
+      // 32-bit slot indices when every slot fits 31 bits
+      const bool idx32 = S < ((int64_t)1 << 31) && env_int("GD_TILE_IDX32", 1) != 0;
+      auto tk = idx32 ? k_c4_tiles<NT, u64, int> : k_c4_tiles<NT, u64, long long>;
+      auto tk32 = idx32 ? k_c4_tiles<NT, unsigned, int> : k_c4_tiles<NT, unsigned, long long>;
       set_smem(tk, sm);
       set_smem(tk32, sm);
       int occ = 0;
