@@ -61,7 +61,29 @@ def build(verbose: bool = False, force: bool = False, defines=(), lib: Path = LI
                *map(str, objs), "-o", str(tmp), "-lcudart_static", "-lrt", "-ldl", "-lpthread", "-lgomp"]
         run(cmd)
         os.replace(tmp, LIB)
+    build_hostpack(force)
     return LIB
+
+
+def hostpack_path() -> Path:
+    import sysconfig
+    return PKG / ("_hostpack" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_hostpack(force: bool = False) -> Path:
+    """The CPython helper that gathers per-graph array pointers for batches
+    (csrc/hostpack.c): plain gcc against this interpreter's headers."""
+    import sysconfig
+    src, out = CSRC / "hostpack.c", hostpack_path()
+    if force or _needs(out, [src]):
+        tmp = out.with_suffix(".tmp")
+        cmd = [os.environ.get("CC", "gcc"), "-O2", "-shared", "-fPIC", "-fvisibility=hidden",
+               f"-I{sysconfig.get_paths()['include']}", str(src), "-o", str(tmp)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"gcc failed:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+        os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

@@ -1208,21 +1208,54 @@ k_c4_flow(View g, const int64_t* __restrict__ WP, FlowPlan P, unsigned* __restri
 // (w, [a, b))), prefix their lengths with a warp scan and walk the items
 // lane-interleaved (consecutive lanes read consecutive slots of one row w).
 // ------------------------------------------------------------------------
+// Tiles have degree-aware widths: a counter of x never exceeds deg(x) (its
+// wedges s-w-x need w in N(x)), and ranks ascend by degree, so a tile whose
+// highest rank has degree < 2^b packs b-bit counters (b = 2, 4, 8, 16) and
+// spans 16/b times the ranks of a 16-bit tile in the same shared memory.  Tiles
+// of one width form a run of equal spans (the last one cut at the degree
+// limit); at most four runs, ascending widths.
+struct TileRuns {
+  int R[4];  // first rank of the run (INT_MAX: unused)
+  int T[4];  // ranks per tile
+  int I[4];  // index of the run's first tile
+  __host__ __device__ __forceinline__ int tile_of(int x) const {
+    const int r = (x >= R[1]) + (x >= R[2]) + (x >= R[3]);
+    const int R0 = r == 0 ? R[0] : r == 1 ? R[1] : r == 2 ? R[2] : R[3];
+    const int T0 = r == 0 ? T[0] : r == 1 ? T[1] : r == 2 ? T[2] : T[3];
+    const int I0 = r == 0 ? I[0] : r == 1 ? I[1] : r == 2 ? I[2] : I[3];
+    return I0 + (x - R0) / T0;
+  }
+};
+
 struct TilePlan {
   const int* frames;    // heavy frames (rank ids), descending wedges
   const int64_t* jpre;  // [nf+1] job prefix: frame j owns jobs [jpre[j], jpre[j+1])
   const int* jframe;    // [njobs] frame of each job
   int nf;
   int64_t njobs;
-  int x0;               // first counter rank (even)
-  int T;                // counters per tile (multiple of 8)
-  int P1;               // split entries per row (tiles of [x0, n) + 1)
-  const int64_t* TS;    // [n][P1] absolute slot of the first entry >= x0 + p*T
+  int cap16;            // shared-memory tile capacity in 16-bit units (multiple of 8)
+  int P1;               // split entries per row (tiles + 1)
+  const int64_t* TS;    // [n][P1] absolute slot of the first entry >= tb[p]
+  const int* tb;        // [P1] first rank of tile p (tb[P1-1] = n)
+  const int* tlg;       // [P1-1] log2 of the counter bits of tile p (1..4)
 };
 
-// TS[w][p] = rp[w] + #(entries of row w with rank < x0 + p*T), warp per row:
+// first rank whose degree exceeds 0, 3, 15, 255 (ranks ascend by degree)
+__global__ void k_degree_ranks(View g, int* __restrict__ out) {
+  const int lim[4] = {0, 3, 15, 255};
+  if (threadIdx.x < 4) {
+    int64_t lo = 0, hi = g.n;  // first r in [0, n] with deg[r] > lim
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (g.deg[mid] > lim[threadIdx.x]) hi = mid; else lo = mid + 1;
+    }
+    out[threadIdx.x] = (int)lo;
+  }
+}
+
+// TS[w][p] = rp[w] + #(entries of row w with rank < tb[p]), warp per row:
 // lane j marks the tiles that start at entry j (tile(x_{j-1}) < p <= tile(x_j)).
-__global__ void k_tile_splits(View g, int x0, int T, int P1, int64_t* __restrict__ TS) {
+__global__ void k_tile_splits(View g, TileRuns RN, int P1, int64_t* __restrict__ TS) {
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int lane = lane_id();
   for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < g.n; w += warps) {
@@ -1231,7 +1264,7 @@ __global__ void k_tile_splits(View g, int x0, int T, int P1, int64_t* __restrict
     int last = -1;  // tile of the last entry seen (all lanes)
     for (int64_t c = b; c < e; c += 32) {
       const int64_t q = c + lane;
-      const int t = q < e ? (g.col[q] - x0) / T : INT_MAX;
+      const int t = q < e ? RN.tile_of(g.col[q]) : INT_MAX;
       int prev = __shfl_up_sync(0xffffffffu, t, 1);
       if (lane == 0) prev = last;
       if (q < e)
@@ -1347,7 +1380,6 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
     typename BR::TempStorage red;
   } tmp;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const unsigned short* tile16 = (const unsigned short*)tile;
   if (threadIdx.x == 0) s_next = (long long)atomicAdd(next_job, 1ull);
   while (true) {
     __syncthreads();
@@ -1361,10 +1393,13 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
     const int s = P.frames[fj];
     const int p = (int)(job - P.jpre[fj]);
     const bool last = job + 1 == P.jpre[fj + 1];  // tile holding rank s - 1: items capped at s
-    const int X = P.x0 + p * P.T;
+    const int X = P.tb[p];
+    // counter width of this tile: 2^lgb bits, 2^csh counters per 32-bit word
+    const int lgb = P.tlg[p], csh = 5 - lgb;
+    const unsigned cmask = (1u << csh) - 1u, vmask = 0xffffffffu >> (32 - (1 << lgb));
     const int64_t b = g.rp[s], nseg = g.osplit[s] - b;
     uint4* t4 = (uint4*)tile;
-    for (int i = threadIdx.x; i < P.T / 8; i += NT) t4[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = threadIdx.x; i < P.cap16 / 8; i += NT) t4[i] = make_uint4(0u, 0u, 0u, 0u);
     u64 local = 0;
     for (int sweep = 0; sweep < (per_edge ? 2 : 1); sweep++) {
       for (int64_t c0 = 0; c0 < nseg; c0 += C) {
@@ -1420,8 +1455,8 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
             tile_range_items<U>(g, seg_pre, seg_off, ncomp, r0, r1,
                                 [&](int k, QT, int x, unsigned) {
                                   if (k >= 0) {
-                                    const int xr = x - X;
-                                    atomicAdd(&tile[xr >> 1], 1u << ((xr & 1) << 4));
+                                    const unsigned xr = (unsigned)(x - X);
+                                    atomicAdd(&tile[xr >> csh], 1u << ((xr & cmask) << lgb));
                                   }
                                 });
           } else {
@@ -1434,7 +1469,8 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
             tile_range_items<U>(g, seg_pre, seg_off, ncomp, r0, r1,
                                 [&](int k, QT q, int x, unsigned) {
               if (k < 0) return;
-              const SumT c = (SumT)((unsigned)tile16[x - X] - 1u);
+              const unsigned xr = (unsigned)(x - X);
+              const SumT c = (SumT)(((tile[xr >> csh] >> ((xr & cmask) << lgb)) & vmask) - 1u);
               if (c) red_add(&c4s[q], (CT)c);  // edge w-x
               if (k != cur_k) {
                 if (cur) atomicAdd(&seg_sum[cur_k], cur);
@@ -1449,7 +1485,8 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
                                 [&](int k, QT q, int x, unsigned M) {
               SumT c = 0;
               if (k >= 0) {
-                c = (SumT)((unsigned)tile16[x - X] - 1u);
+                const unsigned xr = (unsigned)(x - X);
+                c = (SumT)(((tile[xr >> csh] >> ((xr & cmask) << lgb)) & vmask) - 1u);
                 if (c) red_add(&c4s[q], (CT)c);  // edge w-x
               }
               // per-run sums of the step (runs of one segment end where the
@@ -1483,13 +1520,17 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
       }
     }
     if (!per_edge) {  // 2*C(c,2) over the tile's counters
-      for (int i = threadIdx.x; i < P.T / 8; i += NT) {
+      const int bits = 1 << lgb;
+      for (int i = threadIdx.x; i < P.cap16 / 8; i += NT) {
         const uint4 w4 = t4[i];
         const unsigned wv[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
         for (int t = 0; t < 4; t++) {
-          const u64 c0 = wv[t] & 0xffffu, c1 = wv[t] >> 16;
-          local += c0 * (c0 - (c0 > 0)) + c1 * (c1 - (c1 > 0));
+          if (!wv[t]) continue;
+          for (int k = 0; k < 32; k += bits) {
+            const u64 c = (wv[t] >> k) & vmask;
+            local += c * (c - (c > 0));
+          }
         }
       }
     }
@@ -1497,12 +1538,6 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
     const u64 sum = BR(tmp.red).Sum(local);
     if (threadIdx.x == 0 && sum) atomic_add_u128(c4tot2 + 2 * graph_of(g, s), sum);
   }
-}
-
-// number of isolated vertices: they hold the lowest ranks (degree 0)
-__global__ void k_isolated(View g, int* __restrict__ out) {
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r < g.n && g.deg[r] == 0 && (r + 1 == g.n || g.deg[r + 1] > 0)) *out = (int)(r + 1);
 }
 
 // ------------------------------------------------------------------------
@@ -2614,6 +2649,8 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   stat("wedges", total_w);
   stat("tri_items", tot_items);
   int64_t t0 = 256, ta = 1024, t1 = 4096, tb = 12288, t2 = 24576;
+  t2 = env_int("GD_C4_HEAVY_MIN", t2);  // frames above t2 wedges take the heavy-frame path
+  tb = std::min(tb, t2), t1 = std::min(t1, t2), ta = std::min(ta, t2), t0 = std::min(t0, t2);
   if (force.c4_coop || force.c4_hub32 || force.c4_flow) t0 = ta = t1 = tb = t2 = 0;
   if (force.c4_smem) t0 = ta = t1 = 0;  // every frame <= t2 through the u16 hashes
   const auto wr = wk.ranges({{1, t0}, {t0 + 1, ta}, {ta + 1, t1}, {t1 + 1, tb}, {tb + 1, t2},
@@ -2646,14 +2683,14 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     // counters cover ranks [x0, n): isolated vertices (the lowest ranks)
     // never end a wedge
     int x0 = 0;
+    int drank[4] = {0, 0, 0, 0};  // first rank with degree > 0, 3, 15, 255
     if (!f16_all.empty()) {
-      int* d0 = ws_get<int>(g, "x0", 1, s);
-      GD_CUDA(cudaMemsetAsync(d0, 0, 4, s));
-      k_isolated<<<grid_cap(n, 256), 256, 0, s>>>(v, d0);
-      GD_LAUNCH_CHECK("isolated");
-      GD_CUDA(cudaMemcpyAsync(&x0, d0, 4, cudaMemcpyDeviceToHost, s));
+      int* d0 = ws_get<int>(g, "x0", 4, s);
+      k_degree_ranks<<<1, 32, 0, s>>>(v, d0);
+      GD_LAUNCH_CHECK("degree_ranks");
+      GD_CUDA(cudaMemcpyAsync(drank, d0, 16, cudaMemcpyDeviceToHost, s));
       GD_CUDA(cudaStreamSynchronize(s));
-      x0 &= ~1;
+      x0 = drank[0] & ~1;
     }
     // x-tiles in shared memory for every heavy frame (the dense-slab flow
     // kernel and the DSMEM cluster kernel stay selectable: GD_C4_TILES=0,
@@ -2696,29 +2733,65 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       // each) per SM can hold beside the kernel's static arrays
       const int T = force.c4_tile64 ? 64 : (int)(env_int("GD_C4_TILE", NT == 1024 ? 90112 : 45056) &
                                                  ~int64_t(7));
-      const int64_t ptot = (n - x0 + T - 1) / T;
+      // degree-aware tiles (TileRuns): from x0 upward, the counter width whose
+      // tile reaches farthest; GD_C4_TILE_BITS=16 keeps uniform 16-bit tiles
+      const int min_bits = (int)env_int("GD_C4_TILE_BITS", 2);
+      TileRuns RN;
+      for (int c = 0; c < 4; c++) RN.R[c] = INT_MAX, RN.T[c] = 1, RN.I[c] = 0;
+      std::vector<int> tb, tlg;
+      {
+        const int64_t lim[4] = {drank[1], drank[2], drank[3], n};  // b = 2, 4, 8, 16
+        int64_t X = x0;
+        int run = -1, run_lg = 0;
+        while (X < n) {
+          int64_t best = -1;
+          int best_lg = 4;
+          for (int lg = 1; lg <= 4; lg++) {
+            if ((1 << lg) < min_bits) continue;
+            const int64_t end = std::min<int64_t>(X + (int64_t)T * (16 >> lg), lim[lg - 1]);
+            if (end > best) best = end, best_lg = lg;
+          }
+          if (run < 0 || best_lg != run_lg) {
+            run++;
+            run_lg = best_lg;
+            RN.R[run] = (int)X;
+            RN.T[run] = T * (16 >> best_lg);
+            RN.I[run] = (int)tb.size();
+          }
+          tb.push_back((int)X);
+          tlg.push_back(best_lg);
+          X = best;
+        }
+        tb.push_back((int)n);
+      }
+      const int64_t ptot = (int64_t)tlg.size();
       const int P1 = (int)ptot + 1;
+      stat("c4_tile_count", ptot);
       int64_t* TS = ws_get<int64_t>(g, "c4_ts", (size_t)n * P1, s);
-      k_tile_splits<<<grid_cap(n * 32, 256), 256, 0, s>>>(v, x0, T, P1, TS);
+      k_tile_splits<<<grid_cap(n * 32, 256), 256, 0, s>>>(v, RN, P1, TS);
       GD_LAUNCH_CHECK("tile_splits");
       std::vector<int64_t> jpre(f16.size() + 1, 0);
       for (size_t j = 0; j < f16.size(); j++)
-        jpre[j + 1] = jpre[j] + (int64_t)((f16[j] - 1 - x0) / T + 1);
+        jpre[j + 1] = jpre[j] + (int64_t)(RN.tile_of(f16[j] - 1) + 1);
       std::vector<int> jframe(jpre.back());
       for (size_t j = 0; j < f16.size(); j++)
         std::fill(jframe.begin() + jpre[j], jframe.begin() + jpre[j + 1], (int)j);
-      DBuf<int> dfr, djf;
+      DBuf<int> dfr, djf, dtb, dtl;
       DBuf<int64_t> djp;
       DBuf<unsigned long long> njob;
       dfr.alloc(f16.size(), s);
       djp.alloc(jpre.size(), s);
       djf.alloc(jframe.size(), s);
+      dtb.alloc(tb.size(), s);
+      dtl.alloc(tlg.size(), s);
       njob.alloc(1, s);
       njob.zero();
       GD_CUDA(cudaMemcpyAsync(dfr.p, f16.data(), f16.size() * 4, cudaMemcpyHostToDevice, s));
       GD_CUDA(cudaMemcpyAsync(djp.p, jpre.data(), jpre.size() * 8, cudaMemcpyHostToDevice, s));
       GD_CUDA(cudaMemcpyAsync(djf.p, jframe.data(), jframe.size() * 4, cudaMemcpyHostToDevice, s));
-      TilePlan TP{dfr.p, djp.p, djf.p, (int)f16.size(), jpre.back(), x0, T, P1, TS};
+      GD_CUDA(cudaMemcpyAsync(dtb.p, tb.data(), tb.size() * 4, cudaMemcpyHostToDevice, s));
+      GD_CUDA(cudaMemcpyAsync(dtl.p, tlg.data(), tlg.size() * 4, cudaMemcpyHostToDevice, s));
+      TilePlan TP{dfr.p, djp.p, djf.p, (int)f16.size(), jpre.back(), T, P1, TS, dtb.p, dtl.p};
       const size_t sm = (size_t)T * 2;
       // 32-bit slot indices when every slot fits 31 bits
       const bool idx32 = S < ((int64_t)1 << 31) && env_int("GD_TILE_IDX32", 1) != 0;

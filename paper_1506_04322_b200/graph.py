@@ -57,6 +57,15 @@ class _Handle:
             self.p = None
 
 
+def _hostpack():
+    """The CPython pointer-gathering helper, or None when it is not built."""
+    try:
+        from . import _hostpack as hp
+        return hp
+    except ImportError:
+        return None
+
+
 def _as_pairs(pairs) -> np.ndarray:
     if isinstance(pairs, np.ndarray) and pairs.dtype == np.int64 and pairs.ndim == 2 and \
             pairs.shape[1] == 2 and pairs.flags.c_contiguous:
@@ -219,13 +228,19 @@ class GraphBatch:
             raise ValueError("pairs_list and n_list differ in length")
         if not len(pairs_list):
             raise ValueError("empty batch")
-        arrs = [_as_pairs(p) for p in pairs_list]
-        offs = np.zeros(len(arrs) + 1, dtype=np.int64)
-        np.cumsum([len(a) for a in arrs], out=offs[1:])
         # the library gathers the per-graph arrays into its page-locked
-        # staging with all host cores (no packing pass here)
-        ptrs = np.fromiter((a.__array_interface__["data"][0] for a in arrs), dtype=np.uint64,
-                           count=len(arrs))
+        # staging with all host cores (no packing pass here); their pointers
+        # and lengths are collected in one C pass (csrc/hostpack.c)
+        arrs = pairs_list if isinstance(pairs_list, list) else list(pairs_list)
+        offs = np.zeros(len(arrs) + 1, dtype=np.int64)
+        ptrs = np.zeros(len(arrs), dtype=np.uint64)
+        hp = _hostpack()
+        if hp is None or hp.gather(arrs, ptrs, offs) >= 0:  # some array needs conversion
+            arrs = [_as_pairs(p) for p in arrs]
+            if hp is None or hp.gather(arrs, ptrs, offs) >= 0:
+                np.cumsum([len(a) for a in arrs], out=offs[1:])
+                ptrs = np.fromiter((a.__array_interface__["data"][0] for a in arrs),
+                                   dtype=np.uint64, count=len(arrs))
         ns = np.ascontiguousarray(np.asarray(n_list, dtype=np.int64))
         out = ctypes.c_void_p()
         N.check(N.lib().gd_graph_create_batch_list(ctypes.c_void_p(ptrs.ctypes.data), N.ptr(offs),

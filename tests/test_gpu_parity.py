@@ -64,7 +64,8 @@ def test_degenerate_graphs():
 FORCED = ["tri_gmem", "tri_small", "tri_blocks", "c4_coop", "c4_hub32", "c4_smem",
           "c4_flow", "tri_gmem,c4_coop", "tri_small,c4_hub32", "wide_slots", "c4_flow,wide_slots",
           "c4_tile64", "c4_coop,c4_tile64", "c4_coop,c4_tile64,wide_slots", "c4_coop,c4_cluster",
-          "c4_coop,c4_flow", "pipeline"]
+          "c4_coop,c4_flow", "pipeline", "c4_coop,c4_tile64,bits16", "c4_coop,c4_tile64,bits8",
+          "c4_tile64,bits4"]
 
 
 def _dense_cases():
@@ -107,6 +108,9 @@ print("ok")
         env = dict(os.environ, GD_SMALL="0")
     if "wide_slots" in force:  # 64-bit per-slot sums even where 32 bits suffice
         env["GD_WIDE_SLOTS"] = "1"
+    if "bits" in force:  # narrowest counter width of the degree-aware pass-C tiles
+        env["GD_C4_TILE_BITS"] = force.split("bits")[1]
+        env["GD_FORCE_PATH"] = force.split(",bits")[0]
     if force == "tri_small,c4_hub32":
         env["GD_HIT_CAP"] = "5000"  # hit-buffer overflow: pass B re-probes some frames
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
