@@ -1240,10 +1240,10 @@ struct TilePlan {
   const int* tlg;       // [P1-1] log2 of the counter bits of tile p (1..4)
 };
 
-// first rank whose degree exceeds 0, 3, 15, 255 (ranks ascend by degree)
+// first rank whose degree exceeds 0, 1, 3, 15, 255 (ranks ascend by degree)
 __global__ void k_degree_ranks(View g, int* __restrict__ out) {
-  const int lim[4] = {0, 3, 15, 255};
-  if (threadIdx.x < 4) {
+  const int lim[5] = {0, 1, 3, 15, 255};
+  if (threadIdx.x < 5) {
     int64_t lo = 0, hi = g.n;  // first r in [0, n] with deg[r] > lim
     while (lo < hi) {
       const int64_t mid = (lo + hi) >> 1;
@@ -1264,7 +1264,11 @@ __global__ void k_tile_splits(View g, TileRuns RN, int P1, int64_t* __restrict__
     int last = -1;  // tile of the last entry seen (all lanes)
     for (int64_t c = b; c < e; c += 32) {
       const int64_t q = c + lane;
-      const int t = q < e ? RN.tile_of(g.col[q]) : INT_MAX;
+      int t = INT_MAX;
+      if (q < e) {  // entries below the first tile (leaves) count as tile -1
+        const int x = g.col[q];
+        t = x < RN.R[0] ? -1 : RN.tile_of(x);
+      }
       int prev = __shfl_up_sync(0xffffffffu, t, 1);
       if (lane == 0) prev = last;
       if (q < e)
@@ -1294,19 +1298,36 @@ __global__ void k_tile_splits(View g, TileRuns RN, int P1, int64_t* __restrict__
 #ifndef GD_TILE_NT
 #define GD_TILE_NT 1024
 #endif
+#ifndef GD_TILE_CLAIMS
+#define GD_TILE_CLAIMS 4
+#endif
 template <int U, typename QT, typename F>
 __device__ __forceinline__ void tile_range_items(const View& g, const int* seg_pre,
                                                  const QT* seg_off, int cnt,
                                                  int r0, int r1, F&& f) {
   const int lane = threadIdx.x & 31;
   const unsigned le = 0xffffffffu >> (31 - lane);  // bits 0..lane
-  // current segment: last k with seg_pre[k] <= r0
+  // current segment: last k with seg_pre[k] <= r0 (seg_pre ascends, seg_pre[0]
+  // = 0 <= r0).  A warp search: the lanes test 32 spread entries, then the 32
+  // entries of the block found (cnt <= 1024): two shared loads and two
+  // ballots instead of a ten-step dependent binary search per claimed range.
+#ifndef GD_TILE_BSEARCH
+  int kc;
+  {
+    const int b = lane << 5;
+    const unsigned m1 = __ballot_sync(0xffffffffu, b < cnt && seg_pre[b] <= r0);
+    const int blk = (__popc(m1) - 1) << 5;  // m1 has bit 0 set
+    const unsigned m2 = __ballot_sync(0xffffffffu, blk + lane < cnt && seg_pre[blk + lane] <= r0);
+    kc = blk + __popc(m2) - 1;
+  }
+#else
   int lo = 0, hi = cnt;
   while (lo < hi - 1) {
     const int mid = (lo + hi) >> 1;
     if (seg_pre[mid] <= r0) lo = mid; else hi = mid;
   }
   int kc = lo;
+#endif
 #ifndef GD_TILE_NOFAST
   // start of the segment after kc (uniform): steps that end before it lie in
   // segment kc and need no resolution
@@ -1412,7 +1433,7 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
           const int64_t* ts = P.TS + (int64_t)w * P.P1 + p;
           a = ts[0];
           e = ts[1];
-          if (last) e = min(e, P.TS[(int64_t)w * P.P1] + (WP[qs + 1] - WP[qs]));
+          if (last) e = min(e, g.rp[w] + (WP[qs + 1] - WP[qs]));
         }
         const int len = e > a ? (int)(e - a) : 0;
 #ifdef GD_TILE_PREFETCH
@@ -1444,7 +1465,9 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
         if (sweep) seg_sum[threadIdx.x] = 0;
         __syncthreads();
         // item ranges claimed dynamically: long segments spread over warps
-        const int R = min(1024, max(64, ((total / (4 * NW)) + 31) & ~31));
+        // GD_TILE_CLAIMS ranges per warp on average (each claim costs a
+        // shared atomic and a segment search)
+        const int R = max(64, ((total / (GD_TILE_CLAIMS * NW)) + 31) & ~31);
         while (true) {
           int r0 = 0;
           if (lane == 0) r0 = atomicAdd(&s_range, R);
@@ -2497,7 +2520,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       // pass A splits the bitmap rows of big frames into column blocks
       // (column blocking of pass A measured slower than global-memory rows at
       // config 5: 309 vs 176 ms, so it is opt-in: GD_TRI_BLOCKED=1)
-      if (bn.gmem && !force.tri_gmem && (trisum || env_int("GD_TRI_BLOCKED", 0))) {
+      if (bn.gmem && !force.tri_gmem && (trisum || env_int("GD_TRI_BLOCKED", 1))) {
         const int W = (cap + 63) / 64;
         for (int nb = 1; nb <= W; nb++) {
           FrameLayout t = make_layout(cap, !trisum, trisum, (W + nb - 1) / nb);
@@ -2649,7 +2672,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   stat("wedges", total_w);
   stat("tri_items", tot_items);
   int64_t t0 = 256, ta = 1024, t1 = 4096, tb = 12288, t2 = 24576;
-  t2 = env_int("GD_C4_HEAVY_MIN", t2);  // frames above t2 wedges take the heavy-frame path
+  t2 = env_int("GD_C4_HEAVY_MIN", 12288);  // frames above t2 wedges take the heavy-frame path
   tb = std::min(tb, t2), t1 = std::min(t1, t2), ta = std::min(ta, t2), t0 = std::min(t0, t2);
   if (force.c4_coop || force.c4_hub32 || force.c4_flow) t0 = ta = t1 = tb = t2 = 0;
   if (force.c4_smem) t0 = ta = t1 = 0;  // every frame <= t2 through the u16 hashes
@@ -2683,12 +2706,12 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     // counters cover ranks [x0, n): isolated vertices (the lowest ranks)
     // never end a wedge
     int x0 = 0;
-    int drank[4] = {0, 0, 0, 0};  // first rank with degree > 0, 3, 15, 255
+    int drank[5] = {0, 0, 0, 0, 0};  // first rank with degree > 0, 1, 3, 15, 255
     if (!f16_all.empty()) {
-      int* d0 = ws_get<int>(g, "x0", 4, s);
+      int* d0 = ws_get<int>(g, "x0", 5, s);
       k_degree_ranks<<<1, 32, 0, s>>>(v, d0);
       GD_LAUNCH_CHECK("degree_ranks");
-      GD_CUDA(cudaMemcpyAsync(drank, d0, 16, cudaMemcpyDeviceToHost, s));
+      GD_CUDA(cudaMemcpyAsync(drank, d0, 20, cudaMemcpyDeviceToHost, s));
       GD_CUDA(cudaStreamSynchronize(s));
       x0 = drank[0] & ~1;
     }
@@ -2740,8 +2763,10 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       for (int c = 0; c < 4; c++) RN.R[c] = INT_MAX, RN.T[c] = 1, RN.I[c] = 0;
       std::vector<int> tb, tlg;
       {
-        const int64_t lim[4] = {drank[1], drank[2], drank[3], n};  // b = 2, 4, 8, 16
-        int64_t X = x0;
+        const int64_t lim[4] = {drank[2], drank[3], drank[4], n};  // b = 2, 4, 8, 16
+        // a wedge ending at a degree-1 vertex closes no 4-cycle (its counter
+        // stays 1): the tiles start at the first rank of degree 2
+        int64_t X = env_int("GD_C4_TILE_LEAVES", 0) ? x0 : drank[1];
         int run = -1, run_lg = 0;
         while (X < n) {
           int64_t best = -1;
@@ -2772,7 +2797,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       GD_LAUNCH_CHECK("tile_splits");
       std::vector<int64_t> jpre(f16.size() + 1, 0);
       for (size_t j = 0; j < f16.size(); j++)
-        jpre[j + 1] = jpre[j] + (int64_t)(RN.tile_of(f16[j] - 1) + 1);
+        jpre[j + 1] = jpre[j] + (f16[j] - 1 < RN.R[0] ? 0 : (int64_t)(RN.tile_of(f16[j] - 1) + 1));
       std::vector<int> jframe(jpre.back());
       for (size_t j = 0; j < f16.size(); j++)
         std::fill(jframe.begin() + jpre[j], jframe.begin() + jpre[j + 1], (int)j);
@@ -2803,7 +2828,8 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tk, NT, sm));
       if (occ < 1) throw Error(GD_ECUDA, "c4 tile kernel cannot be resident");
       const int grid = (int)std::min<int64_t>(jpre.back(), (int64_t)occ * num_sms());
-      if (narrow)
+      if (grid < 1) {  // every wedge of these frames ends at a leaf: nothing to count
+      } else if (narrow)
         tk32<<<grid, NT, sm, s>>>(v, WP.p, TP, pe, (unsigned*)c4s_p, c4tot2.p, njob.p);
       else
         tk<<<grid, NT, sm, s>>>(v, WP.p, TP, pe, c4s_p, c4tot2.p, njob.p);
