@@ -373,10 +373,25 @@ int gd_graph_create_batch_list(const int64_t* const* lists, const int64_t* pair_
     const int64_t k = num_graphs > 0 ? pair_offsets[num_graphs] - pair_offsets[0] : 0;
     if (k < 0 || (num_graphs > 0 && pair_offsets[0] != 0))
       throw Error(GD_EINVAL, "bad pair_offsets");
+    for (int64_t i = 0; i < num_graphs; i++)
+      if (pair_offsets[i + 1] < pair_offsets[i]) throw Error(GD_EINVAL, "bad pair_offsets");
+    // the per-graph arrays are gathered into page-locked staging by all host
+    // cores in blocks of ~8 MB; the DMA of a block runs while the next is gathered
     int64_t* flat = (int64_t*)host_staging((size_t)std::max<int64_t>(k, 1) * 16);
-    gather_pairs(lists, pair_offsets, num_graphs, flat);
-    build_graph_batch(h->g, flat, pair_offsets, n_per_graph, num_graphs, flags & ~GD_INPUT_DEVICE,
-                      h->s);
+    DBuf<long long> dpairs;
+    dpairs.alloc((size_t)std::max<int64_t>(2 * k, 2), h->s);
+    for (int64_t g0 = 0; g0 < num_graphs;) {
+      int64_t g1 = g0 + 1;
+      while (g1 < num_graphs && pair_offsets[g1] - pair_offsets[g0] < (int64_t)(8 << 20) / 16) g1++;
+      gather_pairs(lists, pair_offsets, g0, g1, flat);
+      const int64_t a = pair_offsets[g0], b = pair_offsets[g1];
+      if (b > a)
+        GD_CUDA(cudaMemcpyAsync(dpairs.p + 2 * a, flat + 2 * a, (size_t)(b - a) * 16,
+                                cudaMemcpyHostToDevice, h->s));
+      g0 = g1;
+    }
+    build_graph_batch(h->g, (const int64_t*)dpairs.p, pair_offsets, n_per_graph, num_graphs,
+                      flags | GD_INPUT_DEVICE, h->s);
   });
   if (rc != GD_OK) {
     gd_graph_free(h);

@@ -173,7 +173,8 @@ void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
 void* host_staging(size_t bytes);
 // A second per-thread page-locked block for small per-call results (sums).
 void* host_results(size_t bytes);
-void gather_pairs(const int64_t* const* lists, const int64_t* offs, int64_t G, int64_t* flat);
+void gather_pairs(const int64_t* const* lists, const int64_t* offs, int64_t g0, int64_t g1,
+                  int64_t* flat);
 
 // ---------------------------------------------------------------------------
 // small device helpers

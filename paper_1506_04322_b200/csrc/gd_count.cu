@@ -153,6 +153,20 @@ struct LocalHash {
       h = (h + 1) & hmask;
     }
   }
+  __device__ __forceinline__ bool maybe(int key) const {  // the filter alone
+    const unsigned fb = mhash((unsigned)key, fshift);
+    return (bf[fb >> 5] >> (fb & 31)) & 1u;
+  }
+  __device__ __forceinline__ int find_exact(int key) const {  // the hash alone
+    unsigned h = mhash((unsigned)key, hshift);
+    int k = hk[h];
+    while (k != key) {
+      if (k == -1) return -1;
+      h = (h + 1) & hmask;
+      k = hk[h];
+    }
+    return hv[h];
+  }
   __device__ __forceinline__ int find(int key) const {
     const unsigned fb = mhash((unsigned)key, fshift);
     if (!((bf[fb >> 5] >> (fb & 31)) & 1u)) return -1;
@@ -279,6 +293,83 @@ __device__ __forceinline__ void for_frame_items(const View& g, const int* P, con
 #endif
 }
 
+// Sweep 1 of a triangle frame with the hit path compacted.  About one item
+// in ten is a local edge, so nearly every 32-item step holds one, and running
+// the hash probe, the bitmap updates and the list append inside the item loop
+// executed half of the kernel's instructions with a few lanes active (ncu:
+// 14-17 active lanes per instruction).  Here the item loop only tests the
+// membership filter; the lanes that pass push (j, i) onto a per-warp queue in
+// shared memory, and whenever 32 entries are queued the whole warp takes one
+// each: exact hash lookup, then hit(j, k, i, is_hit) with all lanes converged
+// (hit() may use full-mask warp collectives).
+#ifndef GD_TRI_NO_COMPACT
+#define GD_TRI_COMPACT 1
+#endif
+template <int NT, typename F>
+__device__ __forceinline__ void frame_items_compact(const View& g, const int* P,
+                                                    const int64_t* QB, int D, int total,
+                                                    const LocalHash& H, u64* wq, F&& hit) {
+  constexpr int K = GD_TRI_K;
+  constexpr int NW = NT / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  u64* q64 = wq + warp * 64;
+  int qn = 0, head = 0;  // queued entries and the ring's first one (warp-uniform)
+  // entries leave in arrival order (the hit lists stay in item order, which
+  // keeps the slot atomics of sweep 2 and pass B coalesced)
+  auto drain = [&](int base, int cnt) {
+    int j = 0, i = 0, k = -1;
+    if (lane < cnt) {
+      const u64 e = q64[(base + lane) & 63];
+      j = (int)(e >> 32);
+      i = (int)(unsigned)e;
+      k = H.find_exact(__ldg(g.col + QB[j] + i));
+    }
+    hit(j, k, i, k >= 0);
+  };
+  for (int c0 = warp * 32 * K; c0 < total; c0 += NW * 32 * K) {
+    const int c1 = min(c0 + 32 * K, total);
+    int i = c0 + lane;
+    bool valid = i < c1;
+    int j = 0, pj1 = 0, y = 0;
+    if (valid) {
+      j = find_segment(P, D, i);
+      pj1 = P[j + 1];
+      y = __ldg(g.col + QB[j] + i);
+    }
+    for (int base = c0; base < c1; base += 32) {
+      // the col[] load of the lane's next item is issued before this one is tested
+      const int ni = i + 32;
+      const bool nvalid = ni < c1;
+      int jn = j, yn = 0;
+      if (nvalid) {
+        while (pj1 <= ni) pj1 = P[++jn + 1];
+        yn = __ldg(g.col + QB[jn] + ni);
+      }
+      const bool pass = valid && H.maybe(y);
+      const unsigned m = __ballot_sync(0xffffffffu, pass);
+      if (m) {
+        if (pass)
+          q64[(head + qn + __popc(m & lt)) & 63] = ((u64)(unsigned)j << 32) | (u64)(unsigned)i;
+        qn += __popc(m);
+        if (qn >= 32) {
+          __syncwarp();
+          drain(head, 32);
+          head = (head + 32) & 63;
+          qn -= 32;
+          __syncwarp();
+        }
+      }
+      i = ni;
+      valid = nvalid;
+      j = jn;
+      y = yn;
+    }
+  }
+  __syncwarp();
+  if (qn) drain(head, qn);
+}
+
 // Set bit b of a 64-bit-word bitmap row with a native 32-bit atomicOr (a
 // 64-bit shared-memory atomicOr compiles to a CAS loop).
 __device__ __forceinline__ void set_bit(u64* row, int b) {
@@ -312,7 +403,8 @@ struct HitLists {
 template <int NT>
 __device__ void tri_frame_single(const View& g, int a, char* mem, const FrameLayout& L,
                           const int64_t* __restrict__ OP, u64* __restrict__ tcs,
-                          u64* __restrict__ vT, u64* __restrict__ k4tot, const HitLists& HL) {
+                          u64* __restrict__ vT, u64* __restrict__ k4tot, const HitLists& HL,
+                          u64* wq) {
   __shared__ int nhits;
   __shared__ u64 s_off;
   LocalHash H;
@@ -332,6 +424,22 @@ __device__ void tri_frame_single(const View& g, int a, char* mem, const FrameLay
   const int total = P[D];
   const int hitcap = (hits && D < 65536) ? HL.stage_cap : 0;
   // sweep 1: local adjacency bitmaps (undirected) + the list of local edges
+#ifdef GD_TRI_COMPACT
+  frame_items_compact<NT>(g, P, QB, D, total, H, wq, [&](int j, int k, int i, bool is_hit) {
+    const unsigned hm = __ballot_sync(0xffffffffu, is_hit);
+    if (!hm) return;
+    if (is_hit) {
+      set_bit(rows + j * RS, k);
+      set_bit(rows + k * RS, j);
+    }
+    if (hitcap) {  // warp-aggregated append
+      int h0 = 0;
+      if (lane_id() == 0) h0 = atomicAdd(&nhits, __popc(hm));
+      const int h = __shfl_sync(0xffffffffu, h0, 0) + __popc(hm & ((1u << lane_id()) - 1u));
+      if (is_hit && h < hitcap) hits[h] = pack_hit(j, k, i);
+    }
+  });
+#else
   for_frame_items<NT>(g, P, QB, D, total, [&](int j, int i, int64_t, int y) {
     const int k = H.find(y);
     if (k >= 0) {
@@ -347,6 +455,7 @@ __device__ void tri_frame_single(const View& g, int a, char* mem, const FrameLay
       }
     }
   });
+#endif
   __syncthreads();
   const int nh = nhits;
   const bool listed = hitcap > 0 && nh <= hitcap;
@@ -420,7 +529,8 @@ __device__ void tri_frame_single(const View& g, int a, char* mem, const FrameLay
 template <int NT>
 __device__ void tri_frame(const View& g, int a, char* mem, const FrameLayout& L,
                           const int64_t* __restrict__ OP, u64* __restrict__ tcs,
-                          u64* __restrict__ vT, u64* __restrict__ k4tot, const HitLists& HL) {
+                          u64* __restrict__ vT, u64* __restrict__ k4tot, const HitLists& HL,
+                          u64* wq) {
   __shared__ int nhits;
   __shared__ u64 s_off;
   LocalHash H;
@@ -468,6 +578,37 @@ __device__ void tri_frame(const View& g, int a, char* mem, const FrameLayout& L,
     const int wcnt = (c1 - c0 + 63) >> 6;  // words used in this block
     for (int i = threadIdx.x; i < D * RS; i += NT) rows[i] = 0ull;
     __syncthreads();
+#ifdef GD_TRI_COMPACT
+    if (blk == 0) {
+      // sweep 1 (probing, hit path compacted): bitmap bits + the list of local edges
+      frame_items_compact<NT>(g, P, QB, D, total, H, wq, [&](int j, int k, int i, bool is_hit) {
+        const unsigned hm = __ballot_sync(0xffffffffu, is_hit);
+        if (!hm) return;
+        if (is_hit) set_bits(j, k, c0, c1);
+        if (hitcap) {  // warp-aggregated append
+          int h0 = 0;
+          if (lane_id() == 0) h0 = atomicAdd(&nhits, __popc(hm));
+          const int h = __shfl_sync(0xffffffffu, h0, 0) + __popc(hm & ((1u << lane_id()) - 1u));
+          if (is_hit && h < hitcap) hits[h] = pack_hit(j, k, i);
+        }
+      });
+      __syncthreads();
+      nh = nhits;
+      listed = hitcap > 0 && nh <= hitcap;
+      // persist the list for pass B (exact-size bump allocation)
+      if (HL.buf && threadIdx.x == 0) {
+        u64 off = ~0ull;
+        if (listed && nh > 0) {
+          off = atomicAdd(HL.top, (u64)nh);
+          if (off + (u64)nh > HL.cap) off = ~0ull;
+        }
+        s_off = off;
+        HL.hoff[a] = (int64_t)off;
+        HL.hcnt[a] = (listed && (nh == 0 || off != ~0ull)) ? nh : -1;
+      }
+      __syncthreads();
+    } else
+#endif
     if (blk == 0 || !listed) {
       // sweep 1 (probing): bitmap bits + the list of local edges
       for_frame_items<NT>(g, P, QB, D, total, [&](int j, int i, int64_t, int y) {
@@ -570,12 +711,13 @@ k_tri_frames(View g, const int* __restrict__ frames, int nframes, int rank, int 
              FrameLayout L, char* gslab, const int64_t* __restrict__ OP, u64* __restrict__ tcs,
              u64* __restrict__ vT, u64* __restrict__ k4tot, HitLists HL) {
   extern __shared__ __align__(16) char smem[];
+  __shared__ u64 wq[(NT / 32) * 64];  // per-warp queues of filter passes (frame_items_compact)
   char* mem = GM ? gslab + (size_t)blockIdx.x * L.bytes : smem;
   for (int f = rank + world * blockIdx.x; f < nframes; f += world * gridDim.x) {
     if (BLOCKED)
-      tri_frame<NT>(g, frames[f], mem, L, OP, tcs, vT, k4tot, HL);
+      tri_frame<NT>(g, frames[f], mem, L, OP, tcs, vT, k4tot, HL, wq);
     else
-      tri_frame_single<NT>(g, frames[f], mem, L, OP, tcs, vT, k4tot, HL);
+      tri_frame_single<NT>(g, frames[f], mem, L, OP, tcs, vT, k4tot, HL, wq);
   }
 }
 
@@ -1375,6 +1517,70 @@ __device__ __forceinline__ void tile_range_items(const View& g, const int* seg_p
   }
 }
 
+// Indexed variant for chunks of at most kTileIdxCap items: the chunk setup
+// leaves, per 32-item word w of the chunk, the start bits B[w] of the segments
+// beginning inside it and C[w] = number of segments beginning before item
+// 32w.  A step then needs no search, no warp collective and no state carried
+// from the previous step: lane l of word w is in segment C[w] - 1 +
+// popc(B[w] & bits <= l) (two broadcast shared loads).  Invalid lanes (past
+// r1) get k = -1 and slot 0.  f(k, q, x).
+constexpr int kTileIdxCap = 32768;
+constexpr int kTileIdxWords = kTileIdxCap / 32 + 8;  // + padding read by the last steps
+
+// Shared memory through explicit 32-bit shared-window addresses held in
+// registers: inside these loops the compiler otherwise rebuilds the window
+// base (S2R SR_CgaCtaId + LEA) before every access (SASS of the first
+// version: 8 of a step's 44 instructions).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ unsigned lds_u32(unsigned a) {
+  unsigned v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ long long lds_off(unsigned base, int k, int) {
+  return (long long)(int)lds_u32(base + 4u * (unsigned)k);
+}
+__device__ __forceinline__ long long lds_off(unsigned base, int k, long long) {
+  long long v;
+  asm volatile("ld.shared.s64 %0, [%1];" : "=l"(v) : "r"(base + 8u * (unsigned)k));
+  return v;
+}
+__device__ __forceinline__ void reds_add(unsigned a, unsigned v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void reds_add(unsigned a, unsigned long long v) {
+  asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+
+template <int U, typename QT, typename F>
+__device__ __forceinline__ void tile_items_indexed(const View& g, unsigned sB, unsigned sC,
+                                                   unsigned sOff, int r0, int r1, F&& f) {
+  const int lane = threadIdx.x & 31;
+  const unsigned le = 0xffffffffu >> (31 - lane);  // bits 0..lane
+  for (int base = r0; base < r1; base += 32 * U) {
+    int kk[U];
+    QT qq[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int wb = base + 32 * u;
+      const unsigned w4 = ((unsigned)wb >> 5) << 2;
+      const bool valid = wb + lane < r1;
+      int ks = (int)lds_u32(sC + w4) - 1 + __popc(lds_u32(sB + w4) & le);
+      ks = valid ? ks : 0;  // (past the chunk's last word the index arrays hold stale values)
+      const QT off = (QT)lds_off(sOff, ks, QT());
+      kk[u] = valid ? ks : -1;
+      qq[u] = valid ? (QT)(off + wb + lane) : (QT)0;
+    }
+    int xx[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) xx[u] = __ldg(g.col + qq[u]);
+#pragma unroll
+    for (int u = 0; u < U; u++) f(kk[u], qq[u], xx[u]);
+  }
+}
+
 // QT: slot index type (int when every slot index fits 31 bits: one IMAD.WIDE
 // per address instead of 64-bit adds)
 template <int NT, typename CT, typename QT>
@@ -1394,6 +1600,8 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
   __shared__ int seg_pre[C + 1];
   __shared__ SumT seg_sum[C];
   __shared__ int seg_slot[C];
+  __shared__ unsigned segB[kTileIdxWords];  // indexed chunks: segment start bits per word
+  __shared__ int segC[kTileIdxWords];       // indexed chunks: segments before each word
   typedef cub::BlockScan<long long, NT> BS;
   typedef cub::BlockReduce<u64, NT> BR;
   __shared__ union {
@@ -1401,6 +1609,8 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
     typename BR::TempStorage red;
   } tmp;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned sTile = smem_u32(tile), sB = smem_u32(segB), sC = smem_u32(segC);
+  const unsigned sOff = smem_u32(seg_off), sSum = smem_u32(seg_sum);
   if (threadIdx.x == 0) s_next = (long long)atomicAdd(next_job, 1ull);
   while (true) {
     __syncthreads();
@@ -1446,6 +1656,9 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
                        : "memory");
         }
 #endif
+#ifndef GD_TILE_NOINDEX
+        for (int w = threadIdx.x; w < kTileIdxWords; w += NT) segB[w] = 0u;
+#endif
         // exclusive prefix of (nonempty flag, length) in one scan: nonempty
         // segments get dense indices (a step of 32 items then meets at most
         // 32 segment starts)
@@ -1453,28 +1666,59 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
         BS(tmp.scan).ExclusiveSum(((long long)(len > 0) << 32) | len, pk, tot);
         const int pre = (int)(pk & 0xffffffffll), ci = (int)(pk >> 32);
         const int total = (int)(tot & 0xffffffffll), ncomp = (int)(tot >> 32);
+#ifndef GD_TILE_NOINDEX
+        const bool indexed = true;
+#else
+        const bool indexed = false;
+#endif
         if (len > 0) {
           seg_off[ci] = (QT)(a - pre);
           seg_pre[ci] = pre;
           seg_slot[ci] = (int)(c0 + threadIdx.x);
         }
-        if (threadIdx.x == 0) {
-          seg_pre[ncomp] = total;
-          s_range = 0;
-        }
+        if (threadIdx.x == 0) seg_pre[ncomp] = total;
         if (sweep) seg_sum[threadIdx.x] = 0;
+        // the chunk's items in windows of kTileIdxCap: each window gets its own
+        // word index (segB / segC, relative to the window's first item)
+        for (int v0 = 0; v0 < (indexed ? total : 1); v0 += kTileIdxCap) {
+        const int vl = indexed ? min(total - v0, kTileIdxCap) : total;
+        if (v0) {  // (the first window's segB was zeroed before the scan)
+          __syncthreads();
+          for (int w = threadIdx.x; w < kTileIdxWords; w += NT) segB[w] = 0u;
+          __syncthreads();
+        }
+        if (indexed && len > 0) {
+          const int p = pre - v0, e = p + len;  // the segment's items relative to the window
+          if (e >= 0 && p < vl) {
+            if (p >= 0) atomicOr(&segB[p >> 5], 1u << (p & 31));
+            // words w with 32w in (p, e]: ci + 1 segments begin before item 32w
+            const int wmax = min(e >> 5, (vl - 1) >> 5);
+            for (int w = p < 0 ? 0 : (p >> 5) + 1; w <= wmax; w++) segC[w] = ci + 1;
+          }
+        }
+        if (threadIdx.x == 0) {
+          s_range = v0;
+          if (v0 == 0) segC[0] = 0;
+        }
         __syncthreads();
+        const unsigned sBw = sB - (((unsigned)v0 >> 5) << 2), sCw = sC - (((unsigned)v0 >> 5) << 2);
         // item ranges claimed dynamically: long segments spread over warps
         // GD_TILE_CLAIMS ranges per warp on average (each claim costs a
         // shared atomic and a segment search)
-        const int R = max(64, ((total / (GD_TILE_CLAIMS * NW)) + 31) & ~31);
+        const int R = max(64, ((vl / (GD_TILE_CLAIMS * NW)) + 31) & ~31);
         while (true) {
           int r0 = 0;
           if (lane == 0) r0 = atomicAdd(&s_range, R);
           r0 = __shfl_sync(0xffffffffu, r0, 0);
-          if (r0 >= total) break;
-          const int r1 = min(total, r0 + R);
-          if (sweep == 0) {
+          if (r0 >= v0 + vl) break;
+          const int r1 = min(v0 + vl, r0 + R);
+          if (sweep == 0 && indexed) {
+            // invalid lanes add 0 to word 0: no branch around the atomic
+            tile_items_indexed<U, QT>(g, sBw, sCw, sOff, r0, r1, [&](int k, QT, int x) {
+              const unsigned xr = k >= 0 ? (unsigned)(x - X) : 0u;
+              reds_add(sTile + ((xr >> csh) << 2), (k >= 0 ? 1u : 0u) << ((xr & cmask) << lgb));
+            });
+          } else if (sweep == 0) {
             tile_range_items<U>(g, seg_pre, seg_off, ncomp, r0, r1,
                                 [&](int k, QT, int x, unsigned) {
                                   if (k >= 0) {
@@ -1482,6 +1726,22 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
                                     atomicAdd(&tile[xr >> csh], 1u << ((xr & cmask) << lgb));
                                   }
                                 });
+          } else if (indexed) {
+            int cur_k = -1;
+            SumT cur = 0;
+            tile_items_indexed<U, QT>(g, sBw, sCw, sOff, r0, r1, [&](int k, QT q, int x) {
+              const unsigned xr = k >= 0 ? (unsigned)(x - X) : 0u;
+              const unsigned cnt = (lds_u32(sTile + ((xr >> csh) << 2)) >> ((xr & cmask) << lgb)) & vmask;
+              const SumT c = k >= 0 ? (SumT)(cnt - 1u) : (SumT)0;
+              if (c) red_add(&c4s[q], (CT)c);  // edge w-x
+              if (k != cur_k) {
+                if (cur) reds_add(sSum + (unsigned)sizeof(SumT) * (unsigned)cur_k, cur);
+                cur_k = k;
+                cur = 0;
+              }
+              cur += c;
+            });
+            if (cur) reds_add(sSum + (unsigned)sizeof(SumT) * (unsigned)cur_k, cur);
           } else {
 #ifndef GD_TILE_RUNSCAN
             // per-lane running sum of its current segment, flushed to the
@@ -1532,6 +1792,7 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
 #endif
           }
         }
+        }  // windows
         __syncthreads();
         if (sweep && threadIdx.x < ncomp) {
           const SumT sm = seg_sum[threadIdx.x];

@@ -22,7 +22,7 @@ python tools/ncu_full_json.py /tmp/${R}_full_c3.ncu-rep > gpurun_out/${R}_ncu_fu
 python tools/ncu_source_top.py /tmp/${R}_full_c3.ncu-rep 12 > gpurun_out/${R}_source_c3_per_edge.json
 python tools/profile_census.py c5_chung_lu_4m per_edge > /dev/null 2>&1 && \
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_c4_flow" -c 1 \
+    -k regex:"k_c4_tiles|k_tri_frames<1024" -c 4 \
     -o /tmp/${R}_full_c5 python tools/profile_census.py c5_chung_lu_4m per_edge \
     > gpurun_out/${R}_full_c5.log 2>&1
 python tools/ncu_full_json.py /tmp/${R}_full_c5.ncu-rep > gpurun_out/${R}_ncu_full_c5_per_edge.json
