@@ -370,6 +370,92 @@ __device__ __forceinline__ void frame_items_compact(const View& g, const int* P,
   if (qn) drain(head, qn);
 }
 
+// The same sweep walked row by row.  The item-space loop above spends ~50
+// SASS instructions per 32-item step on the per-lane segment walk (P[] loop,
+// QB[] load, 64-bit slot address) before the filter test.  A frame's rows
+// average hundreds of items, so here a warp's chunk [c0, c1) is cut at the
+// row boundaries inside it and every piece is scanned with warp-uniform
+// bounds and one uniform row pointer: no per-lane search, U loads in flight
+// per lane, and at most one partly filled step per piece.
+#ifndef GD_TRI_RU
+#define GD_TRI_RU 4
+#endif
+template <int NT, typename F>
+__device__ __forceinline__ void frame_items_rows(const View& g, const int* P, const int64_t* QB,
+                                                 int D, int total, const LocalHash& H, u64* wq,
+                                                 F&& hit) {
+  constexpr int K = GD_TRI_K, U = GD_TRI_RU;
+  constexpr int NW = NT / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  u64* q64 = wq + warp * 64;
+  // the queue through a 32-bit shared-window address (see smem_u32 below: the
+  // generic form rebuilds the window base before every store)
+  const unsigned sQ = (unsigned)__cvta_generic_to_shared(q64);
+  int qn = 0, head = 0;  // queued entries and the ring's first one (warp-uniform)
+  auto drain = [&](int base, int cnt) {
+    int j = 0, i = 0, k = -1;
+    if (lane < cnt) {
+      const u64 e = q64[(base + lane) & 63];
+      j = (int)(e >> 32);
+      i = (int)(unsigned)e;
+      k = H.find_exact(__ldg(g.col + QB[j] + i));
+    }
+    hit(j, k, i, k >= 0);
+  };
+  for (int c0 = warp * 32 * K; c0 < total; c0 += NW * 32 * K) {
+    const int c1 = min(c0 + 32 * K, total);
+    int j = find_segment(P, D, c0);
+    int lo = c0;
+    while (lo < c1) {
+      const int hi = min(P[j + 1], c1);
+      if (hi > lo) {
+        // item i of this row lives at rowl[i - lane]
+        const int* __restrict__ rowl = g.col + (QB[j] + lane);
+        for (int base = lo; base < hi; base += 32 * U) {
+          const int* __restrict__ p = rowl + base;
+          const int rem = hi - base - lane;  // this lane's items left in the row: (rem + 31) / 32
+          int y[U];
+#pragma unroll
+          for (int u = 0; u < U; u++) y[u] = rem > 32 * u ? __ldg(p + 32 * u) : 0;
+#pragma unroll
+          for (int u = 0; u < U; u++) {
+            if (base + 32 * u < hi) {
+              const bool pass = rem > 32 * u && H.maybe(y[u]);
+              const unsigned m = __ballot_sync(0xffffffffu, pass);
+              if (m) {
+                if (pass) {
+                  const unsigned a = sQ + 8u * ((unsigned)(head + qn + __popc(m & lt)) & 63u);
+                  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a),
+                               "r"((unsigned)(base + 32 * u + lane)), "r"((unsigned)j)
+                               : "memory");
+                }
+                qn += __popc(m);
+                if (qn >= 32) {
+                  __syncwarp();
+                  drain(head, 32);
+                  head = (head + 32) & 63;
+                  qn -= 32;
+                  __syncwarp();
+                }
+              }
+            }
+          }
+        }
+      }
+      lo = hi;
+      j++;
+    }
+  }
+  __syncwarp();
+  if (qn) drain(head, qn);
+}
+#ifndef GD_TRI_NO_ROWS
+#define GD_TRI_SWEEP1 frame_items_rows
+#else
+#define GD_TRI_SWEEP1 frame_items_compact
+#endif
+
 // Set bit b of a 64-bit-word bitmap row with a native 32-bit atomicOr (a
 // 64-bit shared-memory atomicOr compiles to a CAS loop).
 __device__ __forceinline__ void set_bit(u64* row, int b) {
@@ -425,7 +511,7 @@ __device__ void tri_frame_single(const View& g, int a, char* mem, const FrameLay
   const int hitcap = (hits && D < 65536) ? HL.stage_cap : 0;
   // sweep 1: local adjacency bitmaps (undirected) + the list of local edges
 #ifdef GD_TRI_COMPACT
-  frame_items_compact<NT>(g, P, QB, D, total, H, wq, [&](int j, int k, int i, bool is_hit) {
+  GD_TRI_SWEEP1<NT>(g, P, QB, D, total, H, wq, [&](int j, int k, int i, bool is_hit) {
     const unsigned hm = __ballot_sync(0xffffffffu, is_hit);
     if (!hm) return;
     if (is_hit) {
@@ -581,7 +667,7 @@ __device__ void tri_frame(const View& g, int a, char* mem, const FrameLayout& L,
 #ifdef GD_TRI_COMPACT
     if (blk == 0) {
       // sweep 1 (probing, hit path compacted): bitmap bits + the list of local edges
-      frame_items_compact<NT>(g, P, QB, D, total, H, wq, [&](int j, int k, int i, bool is_hit) {
+      GD_TRI_SWEEP1<NT>(g, P, QB, D, total, H, wq, [&](int j, int k, int i, bool is_hit) {
         const unsigned hm = __ballot_sync(0xffffffffu, is_hit);
         if (!hm) return;
         if (is_hit) set_bits(j, k, c0, c1);
