@@ -482,6 +482,52 @@ struct HitLists {
   int* hcnt;           // [n] frame -> entries, -1 = not persisted
 };
 
+// Walk a hit list, 32 consecutive entries per warp step; the entry of the
+// lane's next step is loaded before this one is processed.  The entries of a
+// step are consecutive local edges in item order, so most of them share their
+// row j: `grp` is the mask of the lanes with this lane's j (lanes past the end
+// stand alone), for one shared-memory atomic per distinct j instead of up to 32
+// serialised on one address.  f(valid, e, h, grp).
+template <int NT, typename F>
+__device__ __forceinline__ void for_hits(const u64* list, int nh, F&& f) {
+  const int lane = threadIdx.x & 31;
+  int h = threadIdx.x;
+  u64 e = h < nh ? list[h] : 0ull;
+  for (int h0 = threadIdx.x & ~31; h0 < nh; h0 += NT, h += NT) {
+    const u64 en = h + NT < nh ? list[h + NT] : 0ull;
+    const bool valid = h < nh;
+    const int key = valid ? (int)(e >> 48) : 0x10000 + lane;
+#ifndef GD_NO_GROUPED
+    const unsigned grp = __match_any_sync(0xffffffffu, key);
+#else
+    const unsigned grp = 1u << lane;
+#endif
+    f(valid, e, h, grp);
+    e = en;
+  }
+}
+// Sum of v over the lanes of grp (every lane of the warp calls it with its own
+// group mask).  The 64-bit form takes values below 2^32.
+__device__ __forceinline__ unsigned group_sum(unsigned grp, unsigned v) {
+#ifndef GD_NO_GROUPED
+  return __reduce_add_sync(grp, v);
+#else
+  return v;
+#endif
+}
+__device__ __forceinline__ u64 group_sum(unsigned grp, u64 v) {
+#ifndef GD_NO_GROUPED
+  const unsigned lo = __reduce_add_sync(grp, (unsigned)v & 0xffffu);
+  const unsigned hi = __reduce_add_sync(grp, (unsigned)(v >> 16));
+  return ((u64)hi << 16) + lo;
+#else
+  return v;
+#endif
+}
+__device__ __forceinline__ bool group_leader(unsigned grp) {
+  return (int)(threadIdx.x & 31) == __ffs(grp) - 1;
+}
+
 // ------------------------------------------------------------------------
 // pass A
 // ------------------------------------------------------------------------
@@ -573,12 +619,20 @@ __device__ void tri_frame_single(const View& g, int a, char* mem, const FrameLay
     __syncthreads();
     const u64 off = HL.buf ? s_off : ~0ull;
     u64* dst = off != ~0ull ? HL.buf + off : nullptr;
-    for (int h = threadIdx.x; h < nh; h += NT) {
-      const u64 e = hits[h];
-      if (dst) dst[h] = e;
+    for_hits<NT>(hits, nh, [&](bool valid, u64 e, int h, unsigned grp) {
       const int j = (int)(e >> 48), k = (int)((e >> 32) & 0xffff), i = (int)(unsigned)e;
-      local_edge(j, k, QB[j] + i);
-    }
+      unsigned c = 0;
+      if (valid) {
+        if (dst) dst[h] = e;
+        const u64* rj = rows + j * RS;
+        const u64* rk = rows + k * RS;
+        for (int w = 0; w < W; w++) c += __popcll(rj[w] & rk[w]);
+        atomicAdd(&tcs[QB[j] + i], (1ull << kTriShift) + c);
+        if (c) atomicAdd(&tri2[k], c);
+      }
+      const unsigned cs = group_sum(grp, c);
+      if (cs && group_leader(grp)) atomicAdd(&tri2[j], cs);
+    });
   } else {
     for_frame_items<NT>(g, P, QB, D, total, [&](int j, int, int64_t q, int y) {
       const int k = H.find(y);
@@ -739,12 +793,21 @@ __device__ void tri_frame(const View& g, int a, char* mem, const FrameLayout& L,
     // common local neighbours are the 4-cliques {a, x_j, x_k, z}
     if (listed) {
       u64* dst = (blk == 0 && HL.buf && s_off != ~0ull) ? HL.buf + s_off : nullptr;
-      for (int h = threadIdx.x; h < nh; h += NT) {
-        const u64 e = hits[h];
-        if (dst) dst[h] = e;
+      for_hits<NT>(hits, nh, [&](bool valid, u64 e, int h, unsigned grp) {
         const int j = (int)(e >> 48), k = (int)((e >> 32) & 0xffff), i = (int)(unsigned)e;
-        local_edge(j, k, QB[j] + i, blk == 0);
-      }
+        unsigned c = 0;
+        if (valid) {
+          if (dst) dst[h] = e;
+          const u64* rj = rows + j * RS;
+          const u64* rk = rows + k * RS;
+          for (int w = 0; w < WB; w++) c += __popcll(rj[w] & rk[w]);
+          const u64 add = (blk == 0 ? (1ull << kTriShift) : 0ull) + c;
+          if (add) atomicAdd(&tcs[QB[j] + i], add);
+          if (c) atomicAdd(&tri2[k], c);
+        }
+        const unsigned cs = group_sum(grp, c);
+        if (cs && group_leader(grp)) atomicAdd(&tri2[j], cs);
+      });
     } else {
       for_frame_items<NT>(g, P, QB, D, total, [&](int j, int, int64_t q, int y) {
         const int k = H.find(y);
@@ -856,11 +919,33 @@ __device__ void trisum_frame(const View& g, int a, char* mem, const FrameLayout&
   const int nh = HL.hcnt ? HL.hcnt[a] : -1;
   if (nh >= 0) {
     const u64* src = HL.buf + HL.hoff[a];
-    for (int h = threadIdx.x; h < nh; h += NT) {
-      const u64 e = src[h];
+    for_hits<NT>(src, nh, [&](bool valid, u64 e, int, unsigned grp) {
       const int j = (int)(e >> 48), k = (int)((e >> 32) & 0xffff), i = (int)(unsigned)e;
-      local_edge(j, k, QB[j] + i);
-    }
+      AccT v0 = 0, v1 = 0, v2 = 0;
+      if (valid) {
+        const int64_t q = QB[j] + i;
+        const u64 t_jk = tcs[q] >> kTriShift;
+        const int tj = tL[j], tk = tL[k];
+        atomicAdd(&tsl[q], (ST)tj);
+        atomicAdd(&tsh[q], (ST)tk);
+        atomicAdd(&tsd[q], (ST)deg_a);
+        atomicAdd(&acc[3 * k], (AccT)tj);
+        atomicAdd(&acc[3 * k + 1], (AccT)t_jk);
+        atomicAdd(&acc[3 * k + 2], (AccT)dL[j]);
+        v0 = (AccT)tk;
+        v1 = (AccT)t_jk;
+        v2 = (AccT)dL[k];
+      }
+      // the row side (a, x_j): one atomic per distinct j of the step
+      v0 = group_sum(grp, v0);
+      v1 = group_sum(grp, v1);
+      v2 = group_sum(grp, v2);
+      if (v2 && group_leader(grp)) {
+        atomicAdd(&acc[3 * j], v0);
+        atomicAdd(&acc[3 * j + 1], v1);
+        atomicAdd(&acc[3 * j + 2], v2);
+      }
+    });
   } else {
     for_frame_items<NT>(g, P, QB, D, total, [&](int j, int, int64_t q, int y) {
       const int k = H.find(y);
