@@ -1054,6 +1054,17 @@ __device__ __forceinline__ void red_add(unsigned long long* a, unsigned long lon
   asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
 }
 
+// red when v != 0, predicated inside the asm (a C++ `if` around an asm
+// volatile becomes a branch with its own reconvergence point)
+__device__ __forceinline__ void red_add_nz(unsigned* a, unsigned v) {
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %1, 0; @p red.relaxed.gpu.global.add.u32 [%0], %1; }"
+               ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_nz(unsigned long long* a, unsigned long long v) {
+  asm volatile("{ .reg .pred p; setp.ne.u64 p, %1, 0; @p red.relaxed.gpu.global.add.u64 [%0], %1; }"
+               ::"l"(a), "l"(v) : "memory");
+}
+
 struct SlabCounter {  // dense u32 counters in global memory
   unsigned* cnt;
   __device__ __forceinline__ void inc(int x) const { red_add(&cnt[x], 1u); }
@@ -1752,6 +1763,66 @@ __device__ __forceinline__ void tile_items_indexed(const View& g, unsigned sB, u
   }
 }
 
+// Piece walk for chunks whose segments are long: the claimed item range
+// [r0, r1) is cut at the segment boundaries inside it and every piece is
+// scanned with warp-uniform bounds and one row pointer (no per-lane segment
+// resolution at all; at most one partly filled step per piece).
+// item(valid, q, x) per lane and step (lanes past the piece get x = xd);
+// piece_end(k) once per piece, converged.
+#ifndef GD_TILE_PIECE_MIN
+#define GD_TILE_PIECE_MIN 256  // average items per segment of a chunk from which pieces are used
+// (measured 16 / 48 / 64 / 128 / 256 / 512: C3 per-edge pass C 33.2 / 28.9 / 27.5 / 25.0 / 23.7 / 25.5 ms,
+// indexed only 28.6; a two-stage pipeline across pieces was slower: 27.9 ms)
+#endif
+template <int U, typename QT, typename FI, typename FE>
+__device__ __forceinline__ void tile_items_pieces(const View& g, unsigned sPre, unsigned sOff,
+                                                  int cnt, int r0, int r1, int xd, FI&& item,
+                                                  FE&& piece_end) {
+  const int lane = threadIdx.x & 31;
+  int kc;  // last k with seg_pre[k] <= r0 (warp search, see tile_range_items)
+  {
+    const int b = lane << 5;
+    const unsigned m1 =
+        __ballot_sync(0xffffffffu, b < cnt && (int)lds_u32(sPre + 4u * (unsigned)b) <= r0);
+    const int blk = (__popc(m1) - 1) << 5;
+    const unsigned m2 = __ballot_sync(
+        0xffffffffu, blk + lane < cnt && (int)lds_u32(sPre + 4u * (unsigned)(blk + lane)) <= r0);
+    kc = blk + __popc(m2) - 1;
+  }
+  int lo = r0;
+  // the bounds of the next piece are loaded while this one is walked (the
+  // arrays have a spare entry past the chunk's last segment)
+  int npre = (int)lds_u32(sPre + 4u * (unsigned)(kc + 1));
+  QT noff = (QT)lds_off(sOff, kc, QT());
+  while (lo < r1) {
+    const int hi = min(npre, r1);
+    const QT off = noff;
+    npre = (int)lds_u32(sPre + 4u * (unsigned)(kc + 2));
+    noff = (QT)lds_off(sOff, kc + 1, QT());
+    const QT ql = off + (QT)lane;  // item i of the segment lives at slot ql + i - lane
+    const int* __restrict__ rowl = g.col + ql;
+    for (int base = lo; base < hi; base += 32 * U) {
+      const int* __restrict__ pp = rowl + base;
+      const int rem = hi - base - lane;
+      int xx[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) xx[u] = rem > 32 * u ? __ldg(pp + 32 * u) : xd;
+#pragma unroll
+      for (int u = 0; u < U; u++)
+        if (base + 32 * u < hi) item(rem > 32 * u, (QT)(ql + base + 32 * u), xx[u]);
+    }
+    piece_end(kc);
+    lo = hi;
+    kc++;
+  }
+}
+
+__device__ __forceinline__ unsigned warp_sum(unsigned v) { return __reduce_add_sync(0xffffffffu, v); }
+__device__ __forceinline__ u64 warp_sum(u64 v) {
+  for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
 // QT: slot index type (int when every slot index fits 31 bits: one IMAD.WIDE
 // per address instead of 64-bit adds)
 template <int NT, typename CT, typename QT>
@@ -1767,8 +1838,8 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
   extern __shared__ __align__(16) unsigned tile[];  // T u16 counters
   __shared__ long long s_job, s_next;
   __shared__ int s_range;
-  __shared__ QT seg_off[C];
-  __shared__ int seg_pre[C + 1];
+  __shared__ QT seg_off[C + 1];
+  __shared__ int seg_pre[C + 2];
   __shared__ SumT seg_sum[C];
   __shared__ int seg_slot[C];
   __shared__ unsigned segB[kTileIdxWords];  // indexed chunks: segment start bits per word
@@ -1781,7 +1852,9 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
   } tmp;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned sTile = smem_u32(tile), sB = smem_u32(segB), sC = smem_u32(segC);
-  const unsigned sOff = smem_u32(seg_off), sSum = smem_u32(seg_sum);
+  unsigned sOff = smem_u32(seg_off), sSum = smem_u32(seg_sum), sPre = smem_u32(seg_pre);
+  unsigned sTileP = sTile;  // opaque copies for the piece walk: kept in registers, not rebuilt
+  asm volatile("" : "+r"(sTileP), "+r"(sOff), "+r"(sSum), "+r"(sPre));
   if (threadIdx.x == 0) s_next = (long long)atomicAdd(next_job, 1ull);
   while (true) {
     __syncthreads();
@@ -1802,6 +1875,10 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
     const int64_t b = g.rp[s], nseg = g.osplit[s] - b;
     uint4* t4 = (uint4*)tile;
     for (int i = threadIdx.x; i < P.cap16 / 8; i += NT) t4[i] = make_uint4(0u, 0u, 0u, 0u);
+    // the word after the counters serves the piece walk's idle lanes: every
+    // counter in it reads 1 (they add 0 to it, and a count of 1 closes no cycle)
+    const int XD = X + ((P.cap16 / 2) << csh);
+    if (threadIdx.x == 0) tile[P.cap16 / 2] = 0xffffffffu / vmask;
     u64 local = 0;
     for (int sweep = 0; sweep < (per_edge ? 2 : 1); sweep++) {
       for (int64_t c0 = 0; c0 < nseg; c0 += C) {
@@ -1827,9 +1904,6 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
                        : "memory");
         }
 #endif
-#ifndef GD_TILE_NOINDEX
-        for (int w = threadIdx.x; w < kTileIdxWords; w += NT) segB[w] = 0u;
-#endif
         // exclusive prefix of (nonempty flag, length) in one scan: nonempty
         // segments get dense indices (a step of 32 items then meets at most
         // 32 segment starts)
@@ -1837,8 +1911,14 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
         BS(tmp.scan).ExclusiveSum(((long long)(len > 0) << 32) | len, pk, tot);
         const int pre = (int)(pk & 0xffffffffll), ci = (int)(pk >> 32);
         const int total = (int)(tot & 0xffffffffll), ncomp = (int)(tot >> 32);
+        // long segments: piece walk; short ones: the per-word segment index
+#ifndef GD_TILE_NOPIECES
+        const bool pieces = (long long)total >= (long long)GD_TILE_PIECE_MIN * ncomp;
+#else
+        const bool pieces = false;
+#endif
 #ifndef GD_TILE_NOINDEX
-        const bool indexed = true;
+        const bool indexed = !pieces;
 #else
         const bool indexed = false;
 #endif
@@ -1853,8 +1933,8 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
         // word index (segB / segC, relative to the window's first item)
         for (int v0 = 0; v0 < (indexed ? total : 1); v0 += kTileIdxCap) {
         const int vl = indexed ? min(total - v0, kTileIdxCap) : total;
-        if (v0) {  // (the first window's segB was zeroed before the scan)
-          __syncthreads();
+        if (indexed) {
+          if (v0) __syncthreads();
           for (int w = threadIdx.x; w < kTileIdxWords; w += NT) segB[w] = 0u;
           __syncthreads();
         }
@@ -1883,7 +1963,25 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
           r0 = __shfl_sync(0xffffffffu, r0, 0);
           if (r0 >= v0 + vl) break;
           const int r1 = min(v0 + vl, r0 + R);
-          if (sweep == 0 && indexed) {
+          if (sweep == 0 && pieces) {
+            tile_items_pieces<U, QT>(g, sPre, sOff, ncomp, r0, r1, XD, [&](bool valid, QT, int x) {
+              const unsigned xr = (unsigned)(x - X);
+              reds_add(sTileP + ((xr >> csh) << 2), (valid ? 1u : 0u) << ((xr & cmask) << lgb));
+            }, [](int) {});
+          } else if (pieces) {
+            SumT acc = 0;
+            tile_items_pieces<U, QT>(g, sPre, sOff, ncomp, r0, r1, XD, [&](bool, QT q, int x) {
+              const unsigned xr = (unsigned)(x - X);
+              const unsigned cnt = (lds_u32(sTileP + ((xr >> csh) << 2)) >> ((xr & cmask) << lgb)) & vmask;
+              const SumT c = (SumT)(cnt - 1u);  // 0 on idle lanes (the spare word)
+              red_add_nz(&c4s[q], (CT)c);  // edge w-x
+              acc += c;
+            }, [&](int k) {
+              const SumT sm = warp_sum(acc);
+              if (sm && lane == 0) reds_add(sSum + (unsigned)sizeof(SumT) * (unsigned)k, sm);
+              acc = 0;
+            });
+          } else if (sweep == 0 && indexed) {
             // invalid lanes add 0 to word 0: no branch around the atomic
             tile_items_indexed<U, QT>(g, sBw, sCw, sOff, r0, r1, [&](int k, QT, int x) {
               const unsigned xr = k >= 0 ? (unsigned)(x - X) : 0u;
@@ -3249,7 +3347,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       GD_CUDA(cudaMemcpyAsync(dtb.p, tb.data(), tb.size() * 4, cudaMemcpyHostToDevice, s));
       GD_CUDA(cudaMemcpyAsync(dtl.p, tlg.data(), tlg.size() * 4, cudaMemcpyHostToDevice, s));
       TilePlan TP{dfr.p, djp.p, djf.p, (int)f16.size(), jpre.back(), T, P1, TS, dtb.p, dtl.p};
-      const size_t sm = (size_t)T * 2;
+      const size_t sm = (size_t)T * 2 + 16;  // + the spare word of the piece walk
       // 32-bit slot indices when every slot fits 31 bits
       const bool idx32 = S < ((int64_t)1 << 31) && env_int("GD_TILE_IDX32", 1) != 0;
       auto tk = idx32 ? k_c4_tiles<NT, u64, int> : k_c4_tiles<NT, u64, long long>;
