@@ -994,36 +994,37 @@ __global__ void k_hit_bound(View g, const int64_t* __restrict__ OP, u64* __restr
 //   lower slot q (w = col[q] < s): position of s in row w = #x in N(w), x < s
 //                                  (pass C items; e2o of the edge is that slot)
 // ------------------------------------------------------------------------
-__global__ void k_slot_items(View g, int64_t* __restrict__ oitems, int64_t* __restrict__ witems,
-                             u64* __restrict__ tri_key, u64* __restrict__ wedge_key,
-                             int* __restrict__ ids_a, int* __restrict__ ids_b) {
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < g.n; r += warps) {
-    const int64_t b = g.rp[r], o = g.osplit[r], e = g.rp[r + 1];
-    u64 wsum = 0;
-    for (int64_t q = b + lane_id(); q < e; q += 32) {
-      const int x = g.col[q];
-      int64_t oi = 0, wi = 0;
-      if (q >= o) {
-        oi = g.rp[x + 1] - g.osplit[x];
-      } else {
-        wi = g.e2o[g.seid[q]] - g.rp[x];
-      }
-      oitems[q] = oi;
-      witems[q] = wi;
-      wsum += (u64)wi;
-    }
-    for (int off = 16; off; off >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, off);
-    if (lane_id() == 0) {
-      const u64 D = (u64)(e - o);
-      tri_key[r] = ~D;  // descending
-      // wedges, with the lowest bit set when counters may exceed 16 bits
-      const u64 big = (o - b) >= 65536 ? 1ull : 0ull;
-      wedge_key[r] = ~((wsum << 1) | big);
-      ids_a[r] = (int)r;
-      ids_b[r] = (int)r;
-    }
-  }
+__global__ void k_slot_items(View g, int64_t S, int64_t* __restrict__ oitems,
+                             int64_t* __restrict__ witems) {
+  // one thread per slot: q is the out-slot of its edge iff e2o[edge] == q
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= S) return;
+  const int x = g.col[q];
+  const int64_t eo = g.e2o[g.seid[q]];
+  int64_t oi = 0, wi = 0;
+  if (eo == q)
+    oi = g.rp[x + 1] - g.osplit[x];  // out-items: the higher-rank neighbours of x
+  else
+    wi = eo - g.rp[x];  // wedges s-x-*: the entries of row x below s
+  oitems[q] = oi;
+  witems[q] = wi;
+}
+
+// Frame sort keys from the scanned prefixes, one thread per row.
+__global__ void k_frame_keys(View g, const int64_t* __restrict__ WP, u64* __restrict__ tri_key,
+                             u64* __restrict__ wedge_key, int* __restrict__ ids_a,
+                             int* __restrict__ ids_b) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= g.n) return;
+  const int64_t b = g.rp[r], o = g.osplit[r], e = g.rp[r + 1];
+  const u64 wsum = (u64)(WP[o] - WP[b]);  // (wedge items sit on the lower slots [b, o))
+  const u64 D = (u64)(e - o);
+  tri_key[r] = ~D;  // descending
+  // wedges, with the lowest bit set when counters may exceed 16 bits
+  const u64 big = (o - b) >= 65536 ? 1ull : 0ull;
+  wedge_key[r] = ~((wsum << 1) | big);
+  ids_a[r] = (int)r;
+  ids_b[r] = (int)r;
 }
 
 // ------------------------------------------------------------------------
@@ -1579,31 +1580,36 @@ __global__ void k_degree_ranks(View g, int* __restrict__ out) {
 
 // TS[w][p] = rp[w] + #(entries of row w with rank < tb[p]), warp per row:
 // lane j marks the tiles that start at entry j (tile(x_{j-1}) < p <= tile(x_j)).
-__global__ void k_tile_splits(View g, TileRuns RN, int P1, int64_t* __restrict__ TS) {
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int lane = lane_id();
-  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < g.n; w += warps) {
+// GS lanes per row: 8 for the rows below degree 256 (most rows hold a few
+// entries; a warp per row ran at 1-2 active lanes), 32 above.
+template <int GS>
+__global__ void k_tile_splits(View g, TileRuns RN, int P1, int64_t* __restrict__ TS, int64_t w0,
+                              int64_t w1) {
+  const auto grp = cg::tiled_partition<GS>(cg::this_thread_block());
+  const int64_t groups = (int64_t)gridDim.x * (blockDim.x / GS);
+  const int lane = (int)grp.thread_rank();
+  for (int64_t w = w0 + (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / GS; w < w1; w += groups) {
     const int64_t b = g.rp[w], e = g.rp[w + 1];
     int64_t* ts = TS + w * P1;
     int last = -1;  // tile of the last entry seen (all lanes)
-    for (int64_t c = b; c < e; c += 32) {
+    for (int64_t c = b; c < e; c += GS) {
       const int64_t q = c + lane;
       int t = INT_MAX;
       if (q < e) {  // entries below the first tile (leaves) count as tile -1
         const int x = g.col[q];
         t = x < RN.R[0] ? -1 : RN.tile_of(x);
       }
-      int prev = __shfl_up_sync(0xffffffffu, t, 1);
+      int prev = grp.shfl_up(t, 1);
       if (lane == 0) prev = last;
       if (q < e)
         for (int p = prev + 1; p <= t && p < P1; p++) ts[p] = q;
-      last = __shfl_sync(0xffffffffu, t, 31);
+      last = grp.shfl(t, GS - 1);
       if (last == INT_MAX) {  // the row ended inside this chunk: its last tile
-        const unsigned valid = __ballot_sync(0xffffffffu, q < e);
-        last = __shfl_sync(0xffffffffu, t, 31 - __clz(valid));
+        const unsigned valid = grp.ballot(q < e);
+        last = grp.shfl(t, 31 - __clz(valid));
       }
     }
-    for (int p = last + 1 + lane; p < P1; p += 32) ts[p] = e;
+    for (int p = last + 1 + lane; p < P1; p += GS) ts[p] = e;
   }
 }
 
@@ -2914,13 +2920,16 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   idb.alloc(n, s);
   GD_CUDA(cudaMemsetAsync(oitems.p + S, 0, 8, s));
   GD_CUDA(cudaMemsetAsync(witems.p + S, 0, 8, s));
-  if (n) {
-    k_slot_items<<<grid_cap(n * 32, 256), 256, 0, s>>>(v, oitems.p, witems.p, tkey.p, wkey.p,
-                                                       ida.p, idb.p);
+  if (S) {
+    k_slot_items<<<(unsigned)((S + 255) / 256), 256, 0, s>>>(v, S, oitems.p, witems.p);
     GD_LAUNCH_CHECK("slot_items");
   }
   exclusive_scan(oitems.p, OP.p, S + 1, s);
   exclusive_scan(witems.p, WP.p, S + 1, s);
+  if (n) {
+    k_frame_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(v, WP.p, tkey.p, wkey.p, ida.p, idb.p);
+    GD_LAUNCH_CHECK("frame_keys");
+  }
   int64_t tot_items = 0;
   if (S) GD_CUDA(cudaMemcpyAsync(&tot_items, OP.p + S, 8, cudaMemcpyDeviceToHost, s));
   DevKeys dk, wk;
@@ -3323,7 +3332,13 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       const int P1 = (int)ptot + 1;
       stat("c4_tile_count", ptot);
       int64_t* TS = ws_get<int64_t>(g, "c4_ts", (size_t)n * P1, s);
-      k_tile_splits<<<grid_cap(n * 32, 256), 256, 0, s>>>(v, RN, P1, TS);
+      {
+        const int64_t wm = std::min<int64_t>(drank[4], n);  // first rank of degree >= 256
+        const int64_t wz = std::min<int64_t>(drank[0], wm);  // isolated vertices: rows never read
+        if (wm > wz)
+          k_tile_splits<8><<<grid_cap((wm - wz) * 8, 256), 256, 0, s>>>(v, RN, P1, TS, wz, wm);
+        if (n > wm) k_tile_splits<32><<<grid_cap((n - wm) * 32, 256), 256, 0, s>>>(v, RN, P1, TS, wm, n);
+      }
       GD_LAUNCH_CHECK("tile_splits");
       std::vector<int64_t> jpre(f16.size() + 1, 0);
       for (size_t j = 0; j < f16.size(); j++)
