@@ -846,6 +846,16 @@ __device__ void tri_frame(const View& g, int a, char* mem, const FrameLayout& L,
   __syncthreads();
 }
 
+// Next frame of this CTA: the c-th claim of rank r is frame r + world * c.
+// (The frame bodies end with a block barrier, so s_claim is free again.)
+__device__ __forceinline__ int claim_frame(unsigned* claim, int* s_claim, int rank, int world) {
+  if (threadIdx.x == 0) *s_claim = (int)atomicAdd(claim, 1u);
+  __syncthreads();
+  const int c = *s_claim;
+  __syncthreads();
+  return rank + world * c;
+}
+
 // GM: frame scratch in a global slab (largest frames); otherwise in shared
 // memory, where keeping the pointer's provenance static lets the compiler
 // emit LDS/STS/ATOMS instead of generic loads.
@@ -858,11 +868,17 @@ template <int NT, bool BLOCKED, bool GM>
 __global__ void GD_TRI_BOUNDS(NT)
 k_tri_frames(View g, const int* __restrict__ frames, int nframes, int rank, int world,
              FrameLayout L, char* gslab, const int64_t* __restrict__ OP, u64* __restrict__ tcs,
-             u64* __restrict__ vT, u64* __restrict__ k4tot, HitLists HL) {
+             u64* __restrict__ vT, u64* __restrict__ k4tot, HitLists HL,
+             unsigned* __restrict__ claim) {
   extern __shared__ __align__(16) char smem[];
   __shared__ u64 wq[(NT / 32) * 64];  // per-warp queues of filter passes (frame_items_compact)
+  __shared__ int s_claim;
   char* mem = GM ? gslab + (size_t)blockIdx.x * L.bytes : smem;
-  for (int f = rank + world * blockIdx.x; f < nframes; f += world * gridDim.x) {
+  // frames are claimed in descending-D order (a static round-robin gives the
+  // first CTAs the largest frame of every round)
+  while (true) {
+    const int f = claim_frame(claim, &s_claim, rank, world);
+    if (f >= nframes) break;
     if (BLOCKED)
       tri_frame<NT>(g, frames[f], mem, L, OP, tcs, vT, k4tot, HL, wq);
     else
@@ -967,11 +983,15 @@ __global__ void __launch_bounds__(NT)
 k_trisum_frames(View g, const int* __restrict__ frames, int nframes, int rank, int world,
                 FrameLayout L, char* gslab, const int64_t* __restrict__ OP,
                 const u64* __restrict__ tcs, ST* __restrict__ tsl, ST* __restrict__ tsh,
-                ST* __restrict__ tsd, HitLists HL) {
+                ST* __restrict__ tsd, HitLists HL, unsigned* __restrict__ claim) {
   extern __shared__ __align__(16) char smem[];
+  __shared__ int s_claim;
   char* mem = GM ? gslab + (size_t)blockIdx.x * L.bytes : smem;
-  for (int f = rank + world * blockIdx.x; f < nframes; f += world * gridDim.x)
+  while (true) {
+    const int f = claim_frame(claim, &s_claim, rank, world);
+    if (f >= nframes) break;
     trisum_frame<NT, AccT, ST>(g, frames[f], mem, L, OP, tcs, tsl, tsh, tsd, HL);
+  }
 }
 
 // Upper bound of the local-edge count of all frames: sum_a min(items_a, C(D_a, 2)).
@@ -1582,34 +1602,47 @@ __global__ void k_degree_ranks(View g, int* __restrict__ out) {
 // lane j marks the tiles that start at entry j (tile(x_{j-1}) < p <= tile(x_j)).
 // GS lanes per row: 8 for the rows below degree 256 (most rows hold a few
 // entries; a warp per row ran at 1-2 active lanes), 32 above.
+// Long rows are cut into segments of kSplitSeg entries (blockIdx.y): a segment
+// needs only the tile of the entry before it, so a hub row of 60,000 entries
+// is not one warp's serial walk.
+constexpr int kSplitSeg = 1024;
 template <int GS>
 __global__ void k_tile_splits(View g, TileRuns RN, int P1, int64_t* __restrict__ TS, int64_t w0,
                               int64_t w1) {
   const auto grp = cg::tiled_partition<GS>(cg::this_thread_block());
   const int64_t groups = (int64_t)gridDim.x * (blockDim.x / GS);
   const int lane = (int)grp.thread_rank();
+  const bool segmented = gridDim.y > 1;
   for (int64_t w = w0 + (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / GS; w < w1; w += groups) {
     const int64_t b = g.rp[w], e = g.rp[w + 1];
+    const int64_t cb = segmented ? b + (int64_t)blockIdx.y * kSplitSeg : b;
+    const int64_t ce = segmented ? (cb + kSplitSeg < e ? cb + kSplitSeg : e) : e;
+    if (cb >= e && (cb > b || blockIdx.y > 0)) continue;  // no such segment
     int64_t* ts = TS + w * P1;
     int last = -1;  // tile of the last entry seen (all lanes)
-    for (int64_t c = b; c < e; c += GS) {
+    if (cb > b) {
+      const int x = g.col[cb - 1];
+      last = x < RN.R[0] ? -1 : RN.tile_of(x);
+    }
+    for (int64_t c = cb; c < ce; c += GS) {
       const int64_t q = c + lane;
       int t = INT_MAX;
-      if (q < e) {  // entries below the first tile (leaves) count as tile -1
+      if (q < ce) {  // entries below the first tile (leaves) count as tile -1
         const int x = g.col[q];
         t = x < RN.R[0] ? -1 : RN.tile_of(x);
       }
       int prev = grp.shfl_up(t, 1);
       if (lane == 0) prev = last;
-      if (q < e)
+      if (q < ce)
         for (int p = prev + 1; p <= t && p < P1; p++) ts[p] = q;
       last = grp.shfl(t, GS - 1);
-      if (last == INT_MAX) {  // the row ended inside this chunk: its last tile
-        const unsigned valid = grp.ballot(q < e);
+      if (last == INT_MAX) {  // the segment ended inside this chunk: its last tile
+        const unsigned valid = grp.ballot(q < ce);
         last = grp.shfl(t, 31 - __clz(valid));
       }
     }
-    for (int p = last + 1 + lane; p < P1; p += GS) ts[p] = e;
+    if (ce == e)  // the row's last segment: the tiles past its last entry
+      for (int p = last + 1 + lane; p < P1; p += GS) ts[p] = e;
   }
 }
 
@@ -3028,6 +3061,12 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     }
     stat("hit_buffer_entries", (int64_t)hit_cap);
   }
+  // one claim counter per frame-kernel launch (frames are claimed dynamically)
+  constexpr int kMaxClaims = 4096;
+  DBuf<unsigned> claims;
+  claims.alloc(kMaxClaims, s);
+  claims.zero();
+  int nclaims = 0;
   auto run_frames = [&](bool trisum) {
     struct B { int64_t lo, hi; int nt; bool gmem; };
     std::vector<B> bins = {{1025, INT64_MAX, 512, true}, {513, 1024, 512, false},
@@ -3118,6 +3157,9 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
         HL.hcnt = hit_cap ? hcnt : nullptr;
       }
       for (const int rk : my_ranks) {
+      // claim counter of this launch (a slot of a zeroed per-census array)
+      if (nclaims >= kMaxClaims) throw Error(GD_EINVAL, "too many frame launches in one census");
+      unsigned* claim = claims.p + nclaims++;
 #define GD_TRISUM_LAUNCH(NTV, ST)                                                            \
   {                                                                                          \
     ST* ql = (ST*)tsl.p;                                                                     \
@@ -3125,30 +3167,30 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
     ST* qd = (ST*)tsd.p;                                                                     \
     if (sp)                                                                                  \
       k_trisum_frames<NTV, true, u64, ST><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, \
-                                                                sp, OP.p, tcs.p, ql, qh, qd, HL); \
+                                                                sp, OP.p, tcs.p, ql, qh, qd, HL, claim); \
     else if (acc32)                                                                          \
       k_trisum_frames<NTV, false, unsigned, ST><<<grid, NTV, sm, s>>>(                        \
-          v, fr, (int)nf, rk, world, L, sp, OP.p, tcs.p, ql, qh, qd, HL);                    \
+          v, fr, (int)nf, rk, world, L, sp, OP.p, tcs.p, ql, qh, qd, HL, claim);             \
     else                                                                                     \
       k_trisum_frames<NTV, false, u64, ST><<<grid, NTV, sm, s>>>(                             \
-          v, fr, (int)nf, rk, world, L, sp, OP.p, tcs.p, ql, qh, qd, HL);                    \
+          v, fr, (int)nf, rk, world, L, sp, OP.p, tcs.p, ql, qh, qd, HL, claim);             \
   }
 #define GD_TRI_LAUNCH(NTV)                                                                   \
   if (!trisum && blocked) {                                                                  \
     if (sp)                                                                                  \
       k_tri_frames<NTV, true, true><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp,   \
-                                                          OP.p, tcs.p, vT.p, k4tot.p, HL);    \
+                                                          OP.p, tcs.p, vT.p, k4tot.p, HL, claim); \
     else                                                                                     \
       k_tri_frames<NTV, true, false><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp,  \
-                                                           OP.p, tcs.p, vT.p, k4tot.p, HL);   \
+                                                           OP.p, tcs.p, vT.p, k4tot.p, HL, claim); \
     GD_LAUNCH_CHECK("tri_frames_blocked");                                                   \
   } else if (!trisum) {                                                                      \
     if (sp)                                                                                  \
       k_tri_frames<NTV, false, true><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp,  \
-                                                           OP.p, tcs.p, vT.p, k4tot.p, HL);   \
+                                                           OP.p, tcs.p, vT.p, k4tot.p, HL, claim); \
     else                                                                                     \
       k_tri_frames<NTV, false, false><<<grid, NTV, sm, s>>>(v, fr, (int)nf, rk, world, L, sp, \
-                                                            OP.p, tcs.p, vT.p, k4tot.p, HL);  \
+                                                            OP.p, tcs.p, vT.p, k4tot.p, HL, claim); \
     GD_LAUNCH_CHECK("tri_frames");                                                           \
   } else {                                                                                   \
     if (narrow)                                                                              \
@@ -3337,7 +3379,11 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
         const int64_t wz = std::min<int64_t>(drank[0], wm);  // isolated vertices: rows never read
         if (wm > wz)
           k_tile_splits<8><<<grid_cap((wm - wz) * 8, 256), 256, 0, s>>>(v, RN, P1, TS, wz, wm);
-        if (n > wm) k_tile_splits<32><<<grid_cap((n - wm) * 32, 256), 256, 0, s>>>(v, RN, P1, TS, wm, n);
+        if (n > wm) {
+          const int nseg = (int)std::min<int64_t>(65535, (g.max_deg + kSplitSeg - 1) / kSplitSeg);
+          const dim3 grid2(grid_cap((n - wm) * 32, 256), std::max(nseg, 1));
+          k_tile_splits<32><<<grid2, 256, 0, s>>>(v, RN, P1, TS, wm, n);
+        }
       }
       GD_LAUNCH_CHECK("tile_splits");
       std::vector<int64_t> jpre(f16.size() + 1, 0);
