@@ -200,11 +200,20 @@ __global__ void k_slot_keys(const int32_t* __restrict__ eu, const int32_t* __res
   }
 }
 
+// Sorted slot keys (row rank << kb | neighbour rank) -> col[], and the two
+// slots of every edge: the out-slot lies in the row of the lower rank.
 __global__ void k_slot_cols(const unsigned long long* __restrict__ keys, int64_t s, int kb,
-                            int32_t* __restrict__ col) {
+                            const int32_t* __restrict__ seid, int32_t* __restrict__ col,
+                            int64_t* __restrict__ e2o, int64_t* __restrict__ e2i) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s;
-       i += (int64_t)gridDim.x * blockDim.x)
-    col[i] = (int32_t)(keys[i] & ((1ull << kb) - 1));
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long key = keys[i];
+    const int32_t c = (int32_t)(key & ((1ull << kb) - 1));
+    const int32_t r = (int32_t)(key >> kb);
+    col[i] = c;
+    const int e = seid[i];
+    if (c > r) e2o[e] = i; else e2i[e] = i;
+  }
 }
 
 __global__ void k_osplit(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
@@ -212,19 +221,6 @@ __global__ void k_osplit(const int64_t* __restrict__ rp, const int32_t* __restri
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
        r += (int64_t)gridDim.x * blockDim.x)
     osplit[r] = lower_bound_dev(col, rp[r], rp[r + 1], (int32_t)(r + 1));
-}
-
-// e2o / e2i: the two slots of every edge (warp per row)
-__global__ void k_edge_slots(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                             const int32_t* __restrict__ seid, int64_t n,
-                             int64_t* __restrict__ e2o, int64_t* __restrict__ e2i) {
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
-    for (int64_t q = rp[r] + (threadIdx.x & 31); q < rp[r + 1]; q += 32) {
-      const int e = seid[q];
-      if (col[q] > r) e2o[e] = q; else e2i[e] = q;
-    }
-  }
 }
 
 __global__ void k_vgraph(const int32_t* __restrict__ r2d, int64_t n,
@@ -394,19 +390,18 @@ void finish_graph(DevGraph& g, DBuf<unsigned long long>& ukeys, int64_t m, int64
     k_slot_keys<<<grid_for(m), 256, 0, s>>>(g.eu.p, g.ev.p, g.d2r.p, m, kb, sk.p, sv.p);
     GD_LAUNCH_CHECK("slot_keys");
     sort_pairs<int32_t>(sk.p, sk2.p, sv.p, g.seid.p, 2 * m, 2 * kb, s);
-    k_slot_cols<<<grid_for(2 * m), 256, 0, s>>>(sk2.p, 2 * m, kb, g.col.p);
+    g.e2o.alloc(m, s);
+    g.e2i.alloc(m, s);
+    k_slot_cols<<<grid_for(2 * m), 256, 0, s>>>(sk2.p, 2 * m, kb, g.seid.p, g.col.p, g.e2o.p,
+                                                g.e2i.p);
     GD_LAUNCH_CHECK("slot_cols");
+  } else {
+    g.e2o.alloc(m, s);
+    g.e2i.alloc(m, s);
   }
-  g.e2o.alloc(m, s);
-  g.e2i.alloc(m, s);
   if (n) {
     k_osplit<<<grid_for(n), 256, 0, s>>>(g.rp.p, g.col.p, n, g.osplit.p);
     GD_LAUNCH_CHECK("osplit");
-    if (m) {
-      k_edge_slots<<<grid_for(n * 32), 256, 0, s>>>(g.rp.p, g.col.p, g.seid.p, n, g.e2o.p,
-                                                   g.e2i.p);
-      GD_LAUNCH_CHECK("edge_slots");
-    }
   }
   GD_CUDA(cudaStreamSynchronize(s));
   if (g.max_deg >= (1 << 24) - 1)
