@@ -149,20 +149,30 @@ def measured_peak():
     return 6650.0, "fallback"
 
 
-def ncu_traffic(config: str, mode: str):
-    """(DRAM bytes of the top kernel per launch, its name / share, DRAM bytes
-    of one whole census) from the committed ncu launch-list summary
-    (profiles/ncu_summary.json, made by tools/ncu_sum.py)."""
+PHASE_KERNELS = {  # census phase -> the kernels it launches (name prefixes)
+    "c4_coop": ("k_c4_tiles", "k_c4_flow", "k_c4_cluster", "k_c4_hub", "k_c4_rounds"),
+    "tri_frames": ("k_tri_frames",),
+}
+
+
+def ncu_traffic(config: str, mode: str, phase: str):
+    """(DRAM bytes of the phase's kernels in one census, the largest of them by
+    time with its share, DRAM bytes of one whole census) from the committed ncu
+    launch-list summary (profiles/ncu_summary.json, made by tools/ncu_sum.py)."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
         return None, None, None
     try:
         e = json.loads(p.read_text())[f"{config}/{mode}"]
-        top = next(iter(e["kernels"].items()))
-        per = top[1]["dram_bytes"] / max(1, top[1]["launches"])
-        return per, {"name": top[0], "share": top[1]["share"], "dram_bytes": per}, \
-            e["census_dram_bytes"]
-    except (KeyError, ValueError, StopIteration):
+        ks = [(k, v) for k, v in e["kernels"].items()
+              if k.startswith(PHASE_KERNELS.get(phase, ()))]
+        if not ks:
+            return None, None, e["census_dram_bytes"]
+        top = max(ks, key=lambda kv: kv[1]["ms"])
+        total = sum(v["dram_bytes"] for _, v in ks)
+        return total, {"name": top[0], "share": top[1]["share"],
+                       "launches": sum(v["launches"] for _, v in ks)}, e["census_dram_bytes"]
+    except (KeyError, ValueError):
         return None, None, None
 
 
@@ -183,7 +193,6 @@ def roofline_block(config, mode, phases, stats, n, m, deg, ms, peak, peak_kind) 
     (the per-edge formulation's bytes, which this algorithm never reads, so it
     may exceed 1 and is not a bound)."""
     per_edge = mode == "per_edge"
-    traffic, ncu_kernel, census_dram = ncu_traffic(config, mode)
     wh = stats.get("c4_heavy_wedges", 0)
     items = stats.get("tri_items", 0)
     models = {
@@ -194,6 +203,7 @@ def roofline_block(config, mode, phases, stats, n, m, deg, ms, peak, peak_kind) 
     dom = max(((k, v) for k, v in phases.items() if k in models), key=lambda kv: kv[1],
               default=("", 0.0))
     alg, model = models.get(dom[0], (0, ""))
+    traffic, ncu_kernel, census_dram = ncu_traffic(config, mode, dom[0])
     t = max(dom[1], 1e-9) / 1e3
     achieved = alg / t / 1e9
     sum_d2 = int(np.dot(deg, deg))
@@ -203,6 +213,7 @@ def roofline_block(config, mode, phases, stats, n, m, deg, ms, peak, peak_kind) 
            "phase_ms": dom[1], "share_of_census": dom[1] / max(ms, 1e-9),
            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
            "algorithmic_bytes": alg, "model": model, "traffic": traffic,
+           "phase_launches": (ncu_kernel or {}).get("launches"),
            "peak_source": peak_kind}
     if traffic:
         out["hbm_measured"] = {

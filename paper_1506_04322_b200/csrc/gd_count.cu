@@ -1780,7 +1780,28 @@ __device__ __forceinline__ void tile_items_indexed(const View& g, unsigned sB, u
                                                    unsigned sOff, int r0, int r1, F&& f) {
   const int lane = threadIdx.x & 31;
   const unsigned le = 0xffffffffu >> (31 - lane);  // bits 0..lane
-  for (int base = r0; base < r1; base += 32 * U) {
+  int base = r0;
+#ifndef GD_TILE_IDX_NOSPLIT
+  // full groups (every range but a window's last is a multiple of 32 items):
+  // no validity selects; f(valid, k, q, x) folds its own on the literal
+  for (; base + 32 * U <= r1; base += 32 * U) {
+    int kk[U];
+    QT qq[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int wb = base + 32 * u;
+      const unsigned w4 = ((unsigned)wb >> 5) << 2;
+      kk[u] = (int)lds_u32(sC + w4) - 1 + __popc(lds_u32(sB + w4) & le);
+      qq[u] = (QT)((QT)lds_off(sOff, kk[u], QT()) + wb + lane);
+    }
+    int xx[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) xx[u] = __ldg(g.col + qq[u]);
+#pragma unroll
+    for (int u = 0; u < U; u++) f(true, kk[u], qq[u], xx[u]);
+  }
+#endif
+  for (; base < r1; base += 32 * U) {  // the ragged last group
     int kk[U];
     QT qq[U];
 #pragma unroll
@@ -1798,7 +1819,7 @@ __device__ __forceinline__ void tile_items_indexed(const View& g, unsigned sB, u
 #pragma unroll
     for (int u = 0; u < U; u++) xx[u] = __ldg(g.col + qq[u]);
 #pragma unroll
-    for (int u = 0; u < U; u++) f(kk[u], qq[u], xx[u]);
+    for (int u = 0; u < U; u++) f(kk[u] >= 0, kk[u], qq[u], xx[u]);
   }
 }
 
@@ -2022,9 +2043,9 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
             });
           } else if (sweep == 0 && indexed) {
             // invalid lanes add 0 to word 0: no branch around the atomic
-            tile_items_indexed<U, QT>(g, sBw, sCw, sOff, r0, r1, [&](int k, QT, int x) {
-              const unsigned xr = k >= 0 ? (unsigned)(x - X) : 0u;
-              reds_add(sTile + ((xr >> csh) << 2), (k >= 0 ? 1u : 0u) << ((xr & cmask) << lgb));
+            tile_items_indexed<U, QT>(g, sBw, sCw, sOff, r0, r1, [&](bool valid, int, QT, int x) {
+              const unsigned xr = valid ? (unsigned)(x - X) : 0u;
+              reds_add(sTileP + ((xr >> csh) << 2), (valid ? 1u : 0u) << ((xr & cmask) << lgb));
             });
           } else if (sweep == 0) {
             tile_range_items<U>(g, seg_pre, seg_off, ncomp, r0, r1,
@@ -2037,10 +2058,10 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
           } else if (indexed) {
             int cur_k = -1;
             SumT cur = 0;
-            tile_items_indexed<U, QT>(g, sBw, sCw, sOff, r0, r1, [&](int k, QT q, int x) {
-              const unsigned xr = k >= 0 ? (unsigned)(x - X) : 0u;
-              const unsigned cnt = (lds_u32(sTile + ((xr >> csh) << 2)) >> ((xr & cmask) << lgb)) & vmask;
-              const SumT c = k >= 0 ? (SumT)(cnt - 1u) : (SumT)0;
+            tile_items_indexed<U, QT>(g, sBw, sCw, sOff, r0, r1, [&](bool valid, int k, QT q, int x) {
+              const unsigned xr = valid ? (unsigned)(x - X) : 0u;
+              const unsigned cnt = (lds_u32(sTileP + ((xr >> csh) << 2)) >> ((xr & cmask) << lgb)) & vmask;
+              const SumT c = valid ? (SumT)(cnt - 1u) : (SumT)0;
               if (c) red_add(&c4s[q], (CT)c);  // edge w-x
               if (k != cur_k) {
                 if (cur) reds_add(sSum + (unsigned)sizeof(SumT) * (unsigned)cur_k, cur);
