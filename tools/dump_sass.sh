@@ -8,7 +8,7 @@ mkdir -p $OUT
 ROOT=$(cd $(dirname $0)/.. && pwd)
 nvcc -O3 -std=c++17 -lineinfo -gencode arch=compute_100a,code=sm_100a --expt-relaxed-constexpr \
   -I$ROOT/include -cubin -o /tmp/gd_count_sass.cubin $ROOT/paper_1506_04322_b200/csrc/gd_count.cu
-for pat in "k_c4_tilesILi1024EjE" "k_tri_framesILi512ELb0ELb0E" "k_trisum_framesILi512ELb0EjjE" \
+for pat in "k_c4_tilesILi1024EjiE" "k_tri_framesILi512ELb0ELb0E" "k_trisum_framesILi512ELb0EjjE" \
            "k_finalize_singleILi256E" "k_c4_flowILi512ELi4ELi1ELi2EjE" "k_small_censusILi256ELb1ELb0E" \
            "k_small_censusILi128ELb0ELb1E" "k_c4_frames_smemILi1024ELb1EjE"; do
   fn=$(cuobjdump -elf /tmp/gd_count_sass.cubin | grep -o "\.text\.[^ ]*$pat[^ ]*" | head -1 | sed 's/^\.text\.//')
