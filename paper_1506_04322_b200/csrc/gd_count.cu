@@ -1583,6 +1583,7 @@ struct TilePlan {
   const int64_t* TS;    // [n][P1] absolute slot of the first entry >= tb[p]
   const int* tb;        // [P1] first rank of tile p (tb[P1-1] = n)
   const int* tlg;       // [P1-1] log2 of the counter bits of tile p (1..4)
+  int piece_min;        // chunks averaging >= this many items per segment take the piece walk
 };
 
 // first rank whose degree exceeds 0, 1, 3, 15, 255 (ranks ascend by degree)
@@ -1830,7 +1831,7 @@ __device__ __forceinline__ void tile_items_indexed(const View& g, unsigned sB, u
 // item(valid, q, x) per lane and step (lanes past the piece get x = xd);
 // piece_end(k) once per piece, converged.
 #ifndef GD_TILE_PIECE_MIN
-#define GD_TILE_PIECE_MIN 256  // average items per segment of a chunk from which pieces are used
+#define GD_TILE_PIECE_MIN 192  // average items per segment of a chunk from which pieces are used
 // (measured 16 / 48 / 64 / 128 / 256 / 512: C3 per-edge pass C 33.2 / 28.9 / 27.5 / 25.0 / 23.7 / 25.5 ms,
 // indexed only 28.6; a two-stage pipeline across pieces was slower: 27.9 ms)
 #endif
@@ -1973,7 +1974,7 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
         const int total = (int)(tot & 0xffffffffll), ncomp = (int)(tot >> 32);
         // long segments: piece walk; short ones: the per-word segment index
 #ifndef GD_TILE_NOPIECES
-        const bool pieces = (long long)total >= (long long)GD_TILE_PIECE_MIN * ncomp;
+        const bool pieces = (long long)total >= (long long)P.piece_min * ncomp;
 #else
         const bool pieces = false;
 #endif
@@ -3428,7 +3429,8 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       GD_CUDA(cudaMemcpyAsync(djf.p, jframe.data(), jframe.size() * 4, cudaMemcpyHostToDevice, s));
       GD_CUDA(cudaMemcpyAsync(dtb.p, tb.data(), tb.size() * 4, cudaMemcpyHostToDevice, s));
       GD_CUDA(cudaMemcpyAsync(dtl.p, tlg.data(), tlg.size() * 4, cudaMemcpyHostToDevice, s));
-      TilePlan TP{dfr.p, djp.p, djf.p, (int)f16.size(), jpre.back(), T, P1, TS, dtb.p, dtl.p};
+      TilePlan TP{dfr.p, djp.p, djf.p, (int)f16.size(), jpre.back(), T, P1, TS, dtb.p, dtl.p,
+                  (int)std::max<int64_t>(1, env_int("GD_C4_PIECE_MIN", GD_TILE_PIECE_MIN))};
       const size_t sm = (size_t)T * 2 + 16;  // + the spare word of the piece walk
       // 32-bit slot indices when every slot fits 31 bits
       const bool idx32 = S < ((int64_t)1 << 31) && env_int("GD_TILE_IDX32", 1) != 0;

@@ -65,7 +65,7 @@ FORCED = ["tri_gmem", "tri_small", "tri_blocks", "c4_coop", "c4_hub32", "c4_smem
           "c4_flow", "tri_gmem,c4_coop", "tri_small,c4_hub32", "wide_slots", "c4_flow,wide_slots",
           "c4_tile64", "c4_coop,c4_tile64", "c4_coop,c4_tile64,wide_slots", "c4_coop,c4_cluster",
           "c4_coop,c4_flow", "pipeline", "c4_coop,c4_tile64,bits16", "c4_coop,c4_tile64,bits8",
-          "c4_tile64,bits4"]
+          "c4_tile64,bits4", "c4_coop,c4_tile64,pieces1", "c4_coop,pieces1", "c4_coop,pieces8,bits16"]
 
 
 def _dense_cases():
@@ -114,6 +114,10 @@ print("ok")
         env = dict(os.environ, GD_SMALL="0")
     if "wide_slots" in force:  # 64-bit per-slot sums even where 32 bits suffice
         env["GD_WIDE_SLOTS"] = "1"
+    if "pieces" in force:  # piece walk of the pass-C tiles from this average segment length
+        env["GD_C4_PIECE_MIN"] = force.split("pieces")[1].split(",")[0]
+        env["GD_FORCE_PATH"] = force.split(",pieces")[0]
+        force = force.replace(",pieces" + env["GD_C4_PIECE_MIN"], "")
     if "bits" in force:  # narrowest counter width of the degree-aware pass-C tiles
         env["GD_C4_TILE_BITS"] = force.split("bits")[1]
         env["GD_FORCE_PATH"] = force.split(",bits")[0]
