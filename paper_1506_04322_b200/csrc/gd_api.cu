@@ -377,6 +377,8 @@ int gd_graph_create_batch_list(const int64_t* const* lists, const int64_t* pair_
       if (pair_offsets[i + 1] < pair_offsets[i]) throw Error(GD_EINVAL, "bad pair_offsets");
     // the per-graph arrays are gathered into page-locked staging by all host
     // cores in blocks of ~8 MB; the DMA of a block runs while the next is gathered
+    static const bool prof = getenv("GD_HOST_PROFILE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     int64_t* flat = (int64_t*)host_staging((size_t)std::max<int64_t>(k, 1) * 16);
     DBuf<long long> dpairs;
     dpairs.alloc((size_t)std::max<int64_t>(2 * k, 2), h->s);
@@ -390,8 +392,17 @@ int gd_graph_create_batch_list(const int64_t* const* lists, const int64_t* pair_
                                 cudaMemcpyHostToDevice, h->s));
       g0 = g1;
     }
+    const auto t1 = std::chrono::steady_clock::now();
+    if (prof) GD_CUDA(cudaStreamSynchronize(h->s));
+    const auto t2 = std::chrono::steady_clock::now();
     build_graph_batch(h->g, (const int64_t*)dpairs.p, pair_offsets, n_per_graph, num_graphs,
                       flags | GD_INPUT_DEVICE, h->s);
+    if (prof) {
+      const auto t3 = std::chrono::steady_clock::now();
+      auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+      fprintf(stderr, "batch_list: gather+issue %.0f us  h2d drain %.0f us  build %.0f us\n",
+              us(t0, t1), us(t1, t2), us(t2, t3));
+    }
   });
   if (rc != GD_OK) {
     gd_graph_free(h);

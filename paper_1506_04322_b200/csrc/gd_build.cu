@@ -238,19 +238,21 @@ __global__ void k_vgraph(const int32_t* __restrict__ r2d, int64_t n,
   }
 }
 
-__global__ void k_edge_graph_count(const int32_t* __restrict__ eu, int64_t m,
-                                   const int64_t* __restrict__ voff, int64_t G,
-                                   int64_t* __restrict__ counts) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t d = eu[e];
-    int64_t lo = 0, hi = G - 1;
-    while (lo < hi) {
-      int64_t mid = (lo + hi + 1) >> 1;
-      if (voff[mid] <= d) lo = mid; else hi = mid - 1;
-    }
-    atomicAdd((unsigned long long*)&counts[lo], 1ull);
+// eoff[g] = first canonical edge of graph g: edges ascend by their lower dense
+// id and the graphs own contiguous id ranges, so it is a lower bound over eu.
+__global__ void k_edge_offsets(const int32_t* __restrict__ eu, int64_t m,
+                               const int64_t* __restrict__ voff, int64_t G,
+                               int64_t* __restrict__ eoff) {
+  const int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gi > G) return;
+  int64_t lo = 0, hi = m;
+  if (gi == G) lo = m;
+  const int64_t v0 = gi < G ? voff[gi] : 0;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)eu[mid] < v0) lo = mid + 1; else hi = mid;
   }
+  eoff[gi] = lo;
 }
 
 __global__ void k_max_int(const int32_t* __restrict__ a, int64_t n, int* out) {
@@ -585,22 +587,13 @@ void build_graph_batch(DevGraph& g, const int64_t* pairs_in, const int64_t* poff
     k_vgraph<<<grid_for(n), 256, 0, s>>>(g.r2d.p, n, d_voff.p, G, g.vgraph.p);
     GD_LAUNCH_CHECK("vgraph");
   }
-  DBuf<int64_t> ecount;
-  ecount.alloc(G, s);
-  ecount.zero();
-  if (m) {
-    k_edge_graph_count<<<grid_for(m), 256, 0, s>>>(g.eu.p, m, d_voff.p, G, ecount.p);
-    GD_LAUNCH_CHECK("edge_graph_count");
-  }
-  std::vector<int64_t> ec(G);
-  GD_CUDA(cudaMemcpyAsync(ec.data(), ecount.p, G * 8, cudaMemcpyDeviceToHost, s));
-  GD_CUDA(cudaStreamSynchronize(s));
-  g.h_eoff.assign(G + 1, 0);
-  for (int64_t i = 0; i < G; i++) g.h_eoff[i + 1] = g.h_eoff[i] + ec[i];
-  g.h_gn.assign(gn_h, gn_h + G);
   g.eoff.alloc(G + 1, s);
   g.gn.alloc(G, s);
-  GD_CUDA(cudaMemcpyAsync(g.eoff.p, g.h_eoff.data(), (G + 1) * 8, cudaMemcpyHostToDevice, s));
+  k_edge_offsets<<<grid_for(G + 1), 256, 0, s>>>(g.eu.p, m, d_voff.p, G, g.eoff.p);
+  GD_LAUNCH_CHECK("edge_offsets");
+  g.h_eoff.assign(G + 1, 0);
+  g.h_gn.assign(gn_h, gn_h + G);
+  GD_CUDA(cudaMemcpyAsync(g.h_eoff.data(), g.eoff.p, (G + 1) * 8, cudaMemcpyDeviceToHost, s));
   GD_CUDA(cudaMemcpyAsync(g.gn.p, g.h_gn.data(), G * 8, cudaMemcpyHostToDevice, s));
   GD_CUDA(cudaStreamSynchronize(s));
 }

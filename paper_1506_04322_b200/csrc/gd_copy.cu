@@ -161,8 +161,8 @@ void* host_staging(size_t bytes) {
 
 void gather_pairs(const int64_t* const* lists, const int64_t* offs, int64_t g0, int64_t g1,
                   int64_t* flat) {
-  const int nt = std::min(8, std::max(1, omp_get_max_threads()));
-#pragma omp parallel for num_threads(nt) schedule(dynamic, 64)
+  const int nt = std::min(16, std::max(1, omp_get_max_threads()));
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 32)
   for (int64_t g = g0; g < g1; g++) {
     const int64_t k = offs[g + 1] - offs[g];
     if (k > 0) std::memcpy(flat + 2 * offs[g], lists[g], (size_t)k * 16);
