@@ -1584,6 +1584,7 @@ struct TilePlan {
   const int* tb;        // [P1] first rank of tile p (tb[P1-1] = n)
   const int* tlg;       // [P1-1] log2 of the counter bits of tile p (1..4)
   int piece_min;        // chunks averaging >= this many items per segment take the piece walk
+  const int2* jobs;     // [njobs] (frame index, tile | last << 16) in processing order
 };
 
 // first rank whose degree exceeds 0, 1, 3, 15, 255 (ranks ascend by degree)
@@ -1925,10 +1926,11 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
     if (job >= P.njobs) break;
     // the next job is claimed now: its latency overlaps this one
     if (threadIdx.x == 0) s_next = (long long)atomicAdd(next_job, 1ull);
-    const int fj = P.jframe[job];
+    const int2 jb = P.jobs[job];
+    const int fj = jb.x;
     const int s = P.frames[fj];
-    const int p = (int)(job - P.jpre[fj]);
-    const bool last = job + 1 == P.jpre[fj + 1];  // tile holding rank s - 1: items capped at s
+    const int p = jb.y & 0xffff;
+    const bool last = (jb.y >> 16) != 0;  // tile holding rank s - 1: items capped at s
     const int X = P.tb[p];
     // counter width of this tile: 2^lgb bits, 2^csh counters per 32-bit word
     const int lgb = P.tlg[p], csh = 5 - lgb;
@@ -3414,6 +3416,32 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       std::vector<int> jframe(jpre.back());
       for (size_t j = 0; j < f16.size(); j++)
         std::fill(jframe.begin() + jpre[j], jframe.begin() + jpre[j + 1], (int)j);
+      // Job order: tile-major, highest tile first.  The jobs in flight at any
+      // time then read the same x-range of the lower rows -- col[] entries of
+      // one tile, 1/4 (C3) to 1/13 (C5) of the array, which stays in L2 -- where
+      // the frame-major order walked whole rows of unrelated frames (at C5
+      // every col[] entry came from DRAM: 689 GB per census).  Within a tile
+      // the frames keep their descending-work order.
+      if (ptot >= 65536) throw Error(GD_EINVAL, "too many pass-C tiles");
+      const int64_t job_order = env_int("GD_C4_JOB_ORDER", 1);
+      std::vector<int2> jobs;
+      jobs.reserve(jpre.back());
+      if (job_order == 0) {
+        for (size_t j = 0; j < f16.size(); j++)
+          for (int64_t q = jpre[j]; q < jpre[j + 1]; q++)
+            jobs.push_back(make_int2((int)j, (int)(q - jpre[j]) | (q + 1 == jpre[j + 1] ? 1 << 16 : 0)));
+      } else {
+        for (int64_t pp = 0; pp < ptot; pp++) {
+          const int64_t tp = job_order == 1 ? ptot - 1 - pp : pp;
+          for (size_t j = 0; j < f16.size(); j++) {
+            const int64_t nt = jpre[j + 1] - jpre[j];
+            if (nt > tp) jobs.push_back(make_int2((int)j, (int)tp | (tp + 1 == nt ? 1 << 16 : 0)));
+          }
+        }
+      }
+      DBuf<int2> djobs;
+      djobs.alloc(jobs.size(), s);
+      GD_CUDA(cudaMemcpyAsync(djobs.p, jobs.data(), jobs.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
       DBuf<int> dfr, djf, dtb, dtl;
       DBuf<int64_t> djp;
       DBuf<unsigned long long> njob;
@@ -3430,7 +3458,7 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
       GD_CUDA(cudaMemcpyAsync(dtb.p, tb.data(), tb.size() * 4, cudaMemcpyHostToDevice, s));
       GD_CUDA(cudaMemcpyAsync(dtl.p, tlg.data(), tlg.size() * 4, cudaMemcpyHostToDevice, s));
       TilePlan TP{dfr.p, djp.p, djf.p, (int)f16.size(), jpre.back(), T, P1, TS, dtb.p, dtl.p,
-                  (int)std::max<int64_t>(1, env_int("GD_C4_PIECE_MIN", GD_TILE_PIECE_MIN))};
+                  (int)std::max<int64_t>(1, env_int("GD_C4_PIECE_MIN", GD_TILE_PIECE_MIN)), djobs.p};
       const size_t sm = (size_t)T * 2 + 16;  // + the spare word of the piece walk
       // 32-bit slot indices when every slot fits 31 bits
       const bool idx32 = S < ((int64_t)1 << 31) && env_int("GD_TILE_IDX32", 1) != 0;
