@@ -252,11 +252,12 @@ def test_config3_rmat20_full_size():
 
 @pytest.mark.slow
 def test_config5_chung_lu_4m_full_size():
-    # the cross-check fixture of this config takes hours of CPU to make
-    # (tools/make_crosscheck_fixtures.py); the oracle samples pin it without
-    g, f = _big_parity("c5_chung_lu_4m", 100,
-                       require_xc=(GOLDEN / "crosscheck_c5_chung_lu_4m.json").exists())
-    assert g.n == 4_000_000
+    # every row of the 64.6M-row table and the 17 counts against the committed
+    # cross-check fixture (4.6 h of CPU, tools/make_crosscheck_fixtures.py),
+    # plus the literal-oracle samples
+    g, f = _big_parity("c5_chung_lu_4m", 100)
+    assert g.n == 4_000_000 and g.m == 64623472
+    assert f.counts["g4_4"] == 1254097230619 and f.counts["g3_1"] == 7146286343
 
 
 @pytest.mark.parametrize("force", ["", "tri_gmem,c4_coop", "c4_hub32"])
