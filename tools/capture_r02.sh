@@ -2,7 +2,7 @@
 # Round-2 evidence: per-kernel DRAM of one census (C3, C5 both modes), full-set
 # metrics of the dominant kernels, and the bench launch list.  Every ncu run
 # follows a plain run of the same command that exited 0.
-cd /root/repo
+cd "$(dirname "$0")/.."
 R=r02
 set -x
 for cfg in c3_rmat20 c5_chung_lu_4m; do
