@@ -272,6 +272,10 @@ static void census(gd_graph* h, bool per_edge, int64_t* table, int flags, uint64
     }
   }
   CensusExtras ex;
+  // a page-locked host table (the default path's pooled blocks) is filled
+  // chunk by chunk from inside the census, overlapped with the finalize
+  if (dtable.p && r0 == 0 && r1 == g.m && G == 1 && !shard.real() && host_is_pinned(table))
+    ex.host_table = table;
   mark("alloc");
   run_census(g, per_edge, tptr, dsums.p, dseen.p, ex, s, shard);
   mark("run_census");
@@ -282,7 +286,8 @@ static void census(gd_graph* h, bool per_edge, int64_t* table, int flags, uint64
   uint64_t* pin = (uint64_t*)host_results((ns + G) * 8);
   GD_CUDA(cudaMemcpyAsync(pin, dsums.p, ns * 8, cudaMemcpyDeviceToHost, s));
   GD_CUDA(cudaMemcpyAsync(pin + ns, dseen.p, G * 8, cudaMemcpyDeviceToHost, s));
-  if (dtable.p && r1 > r0) copy_d2h(table, dtable.p, (size_t)(r1 - r0) * kNumMicro * 8, s);
+  if (dtable.p && r1 > r0 && !ex.table_copied)
+    copy_d2h(table, dtable.p, (size_t)(r1 - r0) * kNumMicro * 8, s);
   GD_CUDA(cudaStreamSynchronize(s));
   mark("d2h");
   store_timings(h, ex);

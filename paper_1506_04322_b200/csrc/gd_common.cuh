@@ -167,6 +167,7 @@ T* ws_get(DevGraph&, const char* name, size_t count, cudaStream_t s) {
 // (gd_copy.cu).  copy_d2h returns when the host buffer holds the data.
 void copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s);
 void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
+bool host_is_pinned(const void* p);  // page-locked (or managed) host memory
 // This thread's page-locked host staging block of at least `bytes` (grown,
 // never shrunk; valid until the next call on the same thread), and the
 // parallel gather of per-graph pair arrays into it.

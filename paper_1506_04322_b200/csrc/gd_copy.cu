@@ -86,6 +86,8 @@ void copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   }
 }
 
+bool host_is_pinned(const void* p) { return is_pinned(p); }
+
 void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   Staging& st = staging();
   if (bytes < kDirect || is_pinned(dst) || !st.ok) {

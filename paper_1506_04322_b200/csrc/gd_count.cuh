@@ -19,6 +19,12 @@ struct CensusExtras {
   bool direct = false;  // small-graph path: sums complete, no 4-clique / 4-cycle totals
   int64_t row0 = 0;   // first canonical edge of the rows written to the table
   int64_t rows = -1;  // rows written (-1: all m)
+  // in: page-locked host destination of the whole per-edge table (optional).
+  // When set, a single-graph census finalizes in row chunks and copies each
+  // chunk to the host on a second stream while the next one is finalized;
+  // out: table_copied says the host table is complete on return.
+  void* host_table = nullptr;
+  bool table_copied = false;
 };
 
 // Multi-GPU census of one graph.  The frames of passes A-C are dealt
