@@ -1831,6 +1831,9 @@ __device__ __forceinline__ void tile_items_indexed(const View& g, unsigned sB, u
 // resolution at all; at most one partly filled step per piece).
 // item(valid, q, x) per lane and step (lanes past the piece get x = xd);
 // piece_end(k) once per piece, converged.
+#ifndef GD_TILE_PU
+#define GD_TILE_PU 8  // col[] loads in flight per lane in the piece walk (4 / 6 / 8: C5 per-edge pass C 203 / 194 / 190 ms)
+#endif
 #ifndef GD_TILE_PIECE_MIN
 #define GD_TILE_PIECE_MIN 192  // average items per segment of a chunk from which pieces are used
 // (measured 16 / 48 / 64 / 128 / 256 / 512: C3 per-edge pass C 33.2 / 28.9 / 27.5 / 25.0 / 23.7 / 25.5 ms,
@@ -2027,13 +2030,13 @@ k_c4_tiles(View g, const int64_t* __restrict__ WP, TilePlan P, int per_edge,
           if (r0 >= v0 + vl) break;
           const int r1 = min(v0 + vl, r0 + R);
           if (sweep == 0 && pieces) {
-            tile_items_pieces<U, QT>(g, sPre, sOff, ncomp, r0, r1, XD, [&](bool valid, QT, int x) {
+            tile_items_pieces<GD_TILE_PU, QT>(g, sPre, sOff, ncomp, r0, r1, XD, [&](bool valid, QT, int x) {
               const unsigned xr = (unsigned)(x - X);
               reds_add(sTileP + ((xr >> csh) << 2), (valid ? 1u : 0u) << ((xr & cmask) << lgb));
             }, [](int) {});
           } else if (pieces) {
             SumT acc = 0;
-            tile_items_pieces<U, QT>(g, sPre, sOff, ncomp, r0, r1, XD, [&](bool, QT q, int x) {
+            tile_items_pieces<GD_TILE_PU, QT>(g, sPre, sOff, ncomp, r0, r1, XD, [&](bool, QT q, int x) {
               const unsigned xr = (unsigned)(x - X);
               const unsigned cnt = (lds_u32(sTileP + ((xr >> csh) << 2)) >> ((xr & cmask) << lgb)) & vmask;
               const SumT c = (SumT)(cnt - 1u);  // 0 on idle lanes (the spare word)
