@@ -123,7 +123,10 @@ GD_API int gd_census_global(gd_graph* g, uint64_t* sums, int64_t* edges_seen);
  * Per-edge census.  Replaces micro_table (census.py:503-518) ->
  * _micro_batch/_micro_edge (census.py:469-475, 190-256).  table: int64
  * [m][10] canonical order (host, or device with GD_OUTPUT_DEVICE); sums and
- * edges_seen as for gd_census_global (may be NULL).
+ * edges_seen as for gd_census_global (may be NULL).  A page-locked host table
+ * (gd_host_alloc) is filled chunk by chunk on a copy stream while the last
+ * rows are still being finalized; a pageable one is staged through
+ * page-locked blocks by the host cores.
  */
 GD_API int gd_census_per_edge(gd_graph* g, int64_t* table, int flags, uint64_t* sums,
                        int64_t* edges_seen);
