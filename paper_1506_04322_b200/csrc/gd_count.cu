@@ -2191,7 +2191,21 @@ struct EdgeIn {
   bool narrow;      // per-slot sums held as u32 (max degree < 65536)
   const u64* vT;
   const u64* vS;
+  const uint4* vrec;  // [n][2] by dense id: {rank, degree, T lo, T hi} {S lo, S hi, -, -}
 };
+
+// Per-vertex record of the finalize, indexed by DENSE id: one 32-byte sector
+// per endpoint instead of four scattered gathers (d2r, deg, T, S).
+__global__ void k_vertex_records(int64_t n, const int32_t* __restrict__ d2r,
+                                 const int32_t* __restrict__ deg, const u64* __restrict__ vT,
+                                 const u64* __restrict__ vS, uint4* __restrict__ vrec) {
+  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  const int r = d2r[d];
+  const u64 T = vT[r], S = vS[r];
+  vrec[2 * d] = make_uint4((unsigned)r, (unsigned)deg[r], (unsigned)T, (unsigned)(T >> 32));
+  vrec[2 * d + 1] = make_uint4((unsigned)S, (unsigned)(S >> 32), 0u, 0u);
+}
 
 __device__ __forceinline__ long long slot_val(const void* p, int64_t q, bool narrow) {
   return narrow ? (long long)((const unsigned*)p)[q] : (long long)((const u64*)p)[q];
@@ -2218,12 +2232,15 @@ __device__ __forceinline__ void add_sums(u128* acc, long long t, long long su, l
 
 // The 10 raw per-edge fields of edge e (RAW_MICRO_FIELDS order).
 __device__ __forceinline__ void edge_row(const EdgeIn& in, int64_t e, long long* row) {
-  const int ru = in.d2r[in.eu[e]], rv = in.d2r[in.ev[e]];
+  const int64_t du_ = in.eu[e], dv_ = in.ev[e];
+  const uint4 ua = __ldg(in.vrec + 2 * du_), ub = __ldg(in.vrec + 2 * du_ + 1);
+  const uint4 va = __ldg(in.vrec + 2 * dv_), vb = __ldg(in.vrec + 2 * dv_ + 1);
+  const int ru = (int)ua.x, rv = (int)va.x;
   const int64_t qo = in.e2o[e];
   const u64 pk = in.tcs[qo];
   const long long t = (long long)(pk >> kTriShift);
   const long long cl = (long long)(pk & kClMask);
-  const long long du = in.deg[ru], dv = in.deg[rv];
+  const long long du = (long long)ua.y, dv = (long long)va.y;
   const long long su = du - 1 - t, sv = dv - 1 - t;
   row[0] = t;
   row[1] = su;
@@ -2235,11 +2252,13 @@ __device__ __forceinline__ void edge_row(const EdgeIn& in, int64_t e, long long*
   const long long sumU = ru < rv ? slo : shi, sumV = ru < rv ? shi : slo;
   const long long tdeg = slot_val(in.tsd, qo, in.narrow);
   const long long tsu = sumU - 2 * cl - t, tsv = sumV - 2 * cl - t, ts = tsu + tsv;
-  const long long uu = (long long)in.vT[ru] - t - cl - tsu;
-  const long long vv = (long long)in.vT[rv] - t - cl - tsv;
+  const long long Tu = (long long)(((u64)ua.w << 32) | ua.z), Tv = (long long)(((u64)va.w << 32) | va.z);
+  const long long Su = (long long)(((u64)ub.y << 32) | ub.x), Sv = (long long)(((u64)vb.y << 32) | vb.x);
+  const long long uu = Tu - t - cl - tsu;
+  const long long vv = Tv - t - cl - tsv;
   const long long c4 = slot_val(in.c4s, qo, in.narrow) + slot_val(in.c4s, in.e2i[e], in.narrow);
   const long long cy = c4 - ts - 2 * cl;
-  const long long sdeg = (long long)in.vS[ru] - dv + (long long)in.vS[rv] - du - 2 * tdeg;
+  const long long sdeg = Su - dv + Sv - du - 2 * tdeg;
   const long long ti = tdeg - 2 * t - 2 * cl - ts;
   const long long si = sdeg - su - sv - ts - 2 * (uu + vv) - 2 * cy;
   row[4] = cy;
@@ -3772,6 +3791,13 @@ void run_census(DevGraph& g, bool per_edge, long long* table_dev, unsigned long 
   in.c4s = per_edge ? c4s.p : nullptr;
   in.vT = vT.p;
   in.vS = vS.p;
+  DBuf<uint4> vrec;
+  vrec.alloc((size_t)std::max<int64_t>(2 * n, 1), s);
+  if (n) {
+    k_vertex_records<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, g.d2r.p, g.deg.p, vT.p, vS.p, vrec.p);
+    GD_LAUNCH_CHECK("vertex_records");
+  }
+  in.vrec = vrec.p;
   GD_CUDA(cudaMemsetAsync(sums_dev, 0, (size_t)G * 2 * kNumSums * 8, s));
   GD_CUDA(cudaMemsetAsync(seen_dev, 0, (size_t)G * 8, s));
   cudaStream_t copy_stream = nullptr;  // set when the table's D2H was started here
