@@ -2276,6 +2276,7 @@ __device__ void block_flush_sums(u128* acc, u64* out) {
   typedef cub::BlockReduce<u64, NT> BR;
   __shared__ typename BR::TempStorage tmp;
   const u64 mask = (1ull << 43) - 1;
+#pragma unroll  // static indices keep the 13 accumulators in registers (208 B of stack otherwise)
   for (int k = 0; k < kNumSums; k++) {
     const u64 l0 = (u64)(acc[k]) & mask;
     const u64 l1 = (u64)(acc[k] >> 43) & mask;
@@ -2312,6 +2313,7 @@ __global__ void __launch_bounds__(NT)
 k_finalize_single(EdgeIn in, int64_t e0, int64_t e1, long long n, long long m,
                   long long* __restrict__ table, u64* __restrict__ sums, u64* __restrict__ seen) {
   u128 acc[kNumSums];
+#pragma unroll
   for (int k = 0; k < kNumSums; k++) acc[k] = 0;
   u64 cnt = 0;
   long long row[kNumMicro];
