@@ -175,3 +175,34 @@ def test_feature_matrix_skips_like_the_reference(monkeypatch):
     assert fm.labels == ["a", "c"]
     fm = A.feature_matrix([object(), object(), object()], labels=["a", "b"])
     assert fm.labels == ["a"] and len(fm.skipped) == 1
+
+
+def test_bench_roofline_block_is_a_bound():
+    """bench.py's roofline block: the kernel and DRAM traffic belong to the
+    phase that dominates the live timings (profiles/ncu_summary.json), the
+    measured HBM fractions never exceed 1 and `frac` is achieved / peak."""
+    import importlib.util
+    import json
+    root = Path(__file__).resolve().parent.parent
+    spec = importlib.util.spec_from_file_location("bench_mod", root / "bench.py")
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    summ = json.loads((root / "profiles" / "ncu_summary.json").read_text())
+    deg = np.full(1000, 30, dtype=np.int64)
+    for (cfg, mode), phases in {
+        ("c3_rmat20", "per_edge"): {"schedule": 1.1, "tri_frames": 12.4, "trisum_frames": 5.3,
+                                    "c4_coop": 19.6, "c4_smem": 2.0, "finalize": 1.4},
+        ("c5_chung_lu_4m", "global"): {"schedule": 3.9, "tri_frames": 184.8, "c4_coop": 116.7,
+                                       "c4_smem": 3.8, "finalize": 1.5},
+    }.items():
+        stats = {"c4_heavy_wedges": 5_570_596_165, "tri_items": 4_423_179_103}
+        ms = sum(phases.values())
+        r = bench.roofline_block(cfg, mode, phases, stats, 1000, 15000, deg, ms, 6457.1, "measured")
+        dom = max(("c4_coop", "tri_frames"), key=lambda k: phases[k])
+        assert r["phase"] == dom and r["bound"] == "hbm"
+        assert r["kernel"].startswith(bench.PHASE_KERNELS[dom])
+        assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-12
+        names = [k for k in summ[f"{cfg}/{mode}"]["kernels"] if k.startswith(bench.PHASE_KERNELS[dom])]
+        assert r["traffic"] == sum(summ[f"{cfg}/{mode}"]["kernels"][k]["dram_bytes"] for k in names)
+        assert 0 < r["hbm_measured"]["kernel_frac"] <= 1.0
+        assert 0 < r["hbm_measured"]["census_frac"] <= 1.0
