@@ -1664,7 +1664,7 @@ __global__ void k_tile_splits(View g, TileRuns RN, int P1, int64_t* __restrict__
 #define GD_TILE_NT 1024
 #endif
 #ifndef GD_TILE_CLAIMS
-#define GD_TILE_CLAIMS 4
+#define GD_TILE_CLAIMS 1  // item ranges per warp and chunk (8 / 4 / 2 / 1: C3 per-edge pass C 21.6 / 19.6 / 18.7 / 18.4 ms)
 #endif
 template <int U, typename QT, typename F>
 __device__ __forceinline__ void tile_range_items(const View& g, const int* seg_pre,
